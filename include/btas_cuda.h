@@ -1,0 +1,177 @@
+/*
+ * btas_cuda.h — C ABI of libbtas_cuda.so, the B200 (sm_100a) tropical-algebra
+ * kernels behind the drop-in `paper_1701_04733_b200` package.
+ *
+ * The reference (`btas`, /root/reference/pkg/src/btas) is pure Python/NumPy
+ * and has no FFI: its replaceable boundary is the Python API of the hot-path
+ * functions.  Each entry point below replaces the compute body of one
+ * reference function (cited per declaration); the Python mirror in
+ * paper_1701_04733_b200/ keeps the reference names, argument meaning and
+ * exceptions and calls these through ctypes.
+ *
+ * Conventions (all entry points):
+ *  - Plain pointers to DEVICE memory, 64-bit sizes / leading dimensions in
+ *    elements, row-major storage.  No torch types cross this boundary.
+ *  - Every call is stream-ordered on the caller's `stream` (a cudaStream_t;
+ *    NULL = legacy default stream).  Calls never allocate device memory and
+ *    never synchronise the host; scratch space is passed in as `workspace`.
+ *  - Return value: BTAS_OK (0) or a BTAS_ERR_* status; the Python layer maps
+ *    statuses to exceptions (btas_status_string gives the text).
+ *  - Storage is "oriented" exactly like the reference (matrix.py:3-7,82-95):
+ *    the symbolic Infinity is stored as +inf under min-plus and -inf under
+ *    max-plus.  int32 storage encodes it as +/-BTAS_I32_INF and keeps finite
+ *    entries strictly inside (-BTAS_I32_LIMIT, BTAS_I32_LIMIT).
+ *  - dev_flags is an int32[BTAS_NUM_FLAGS] device array; kernels only ever
+ *    OR bits into it (set-only, like the reference's saturation flag,
+ *    semiring.py:73-88).
+ */
+#ifndef BTAS_CUDA_H
+#define BTAS_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* btas_stream_t; /* == cudaStream_t */
+
+/* element types of the storage */
+enum { BTAS_F32 = 0, BTAS_I32 = 1, BTAS_F64 = 2 };
+/* semiring kinds (reference SemiringKind, semiring.py:17-29) */
+enum { BTAS_MIN_PLUS = 0, BTAS_MAX_PLUS = 1 };
+
+/* int32 storage encoding of Infinity and the finite-domain limit */
+#define BTAS_I32_INF 0x3FFFFFFF
+#define BTAS_I32_LIMIT (1 << 28)
+
+/* dev_flags slots */
+enum {
+  BTAS_FLAG_CHANGED = 0,   /* output differs from `Cprev` (fixpoint test, apsp.py:161) */
+  BTAS_FLAG_DIAG_NEG = 1,  /* an output diagonal entry is < 0 (apsp.py:125,168,171) */
+  BTAS_FLAG_SATURATED = 2, /* a finite (x) finite product saturated (matrix.py:334-342) */
+  BTAS_FLAG_PATH = 3,      /* OR of (1 << path) for every GEMM path that ran (diagnostics) */
+  BTAS_NUM_FLAGS = 8
+};
+
+/* GEMM kernel paths (bit index in BTAS_FLAG_PATH) */
+enum {
+  BTAS_PATH_FAST32 = 0,  /* f32 FADD2+FMNMX3 / i32 VIADDMNMX */
+  BTAS_PATH_S16X2 = 1,   /* integer operands with |x| < 2^12: VIADDMNMX.S16x2, 2 pairs/instr */
+  BTAS_PATH_CHECKED = 2, /* per-candidate overflow masking (the reference's masked tile) */
+  BTAS_PATH_FAST64 = 3,  /* f64 DADD + min */
+  BTAS_PATH_EMPTY = 4    /* no work (an operand has no rows/cols) */
+};
+
+/* status codes */
+enum {
+  BTAS_OK = 0,
+  BTAS_ERR_INVALID = 1,     /* bad argument (null pointer, negative size, bad dtype/kind) */
+  BTAS_ERR_CUDA = 2,        /* a CUDA runtime call or launch failed */
+  BTAS_ERR_WORKSPACE = 3,   /* workspace too small */
+  BTAS_ERR_UNSUPPORTED = 4  /* combination not supported */
+};
+
+/* Statistics of one ingest/scan pass (written on the device, read by the host). */
+typedef struct btas_stats {
+  unsigned long long nan_count;      /* NaN entries (ingest: rejected, matrix.py:88-89) */
+  unsigned long long neg_inf_count;  /* -inf in symbolic input (ingest: rejected, matrix.py:90-91) */
+  unsigned long long non_integral;   /* finite entries with a fractional part */
+  unsigned long long over_limit;     /* finite |x| >= the dtype's integer limit (matrix.py:98-115) */
+  unsigned long long out_of_range;   /* finite input not representable in the target dtype */
+  unsigned long long finite_count;   /* finite entries */
+  unsigned long long max_abs_key;    /* ordered key of max |finite| (decode with btas_key_to_double) */
+  unsigned long long min_key;        /* ordered key of min finite */
+  unsigned long long max_key;        /* ordered key of max finite */
+} btas_stats;
+
+const char* btas_version(void);
+const char* btas_status_string(int status);
+/* decode an ordered key of btas_stats; returns NaN for the "no finite entry" key */
+double btas_key_to_double(unsigned long long key);
+/* reset a device btas_stats before an ingest/scan */
+int btas_stats_init(btas_stats* stats_dev, btas_stream_t stream);
+
+/* Ingest symbolic-form values (f64 or f32 device array, +inf = Infinity) into
+ * oriented storage of `dst_dtype`: validates (NaN, -inf), normalises -0.0,
+ * orients Infinity per kind, encodes int32, and accumulates statistics.
+ * Replaces TropicalMatrix/TropicalVector construction (matrix.py:82-115,132-156). */
+int btas_ingest(int kind, int src_dtype, const void* src, int64_t numel,
+                int dst_dtype, void* dst, btas_stats* stats_dev, btas_stream_t stream);
+
+/* Statistics of oriented storage (max |finite|, min/max finite): the
+ * saturation screens of matrix.py:297-312 and apsp.py:103-107. */
+int btas_scan(int dtype, const void* x, int64_t numel, btas_stats* stats_dev, btas_stream_t stream);
+
+/* Oriented storage -> oriented float64 (identical to the reference's .data). */
+int btas_to_f64(int dtype, const void* src, int64_t numel, double* dst, btas_stream_t stream);
+
+/* Fill with Infinity (oriented for kind) or a finite value.
+ * TropicalMatrix.filled (matrix.py:158-168). */
+int btas_fill(int dtype, int kind, void* x, int64_t numel, double value, btas_stream_t stream);
+
+/* identity_matrix (matrix.py:257-263): 0 on the diagonal, Infinity elsewhere. */
+int btas_identity(int dtype, int kind, void* d, int64_t ld, int64_t n, btas_stream_t stream);
+
+/* _closure_base (apsp.py:80-90): dst = src with diag <- min(diag, 0). */
+int btas_closure_base(int dtype, const void* src, int64_t lds, void* dst, int64_t ldd, int64_t n,
+                      btas_stream_t stream);
+
+/* ew_add (matrix.py:271-277), for matrices and vectors: out = a (+) b elementwise. */
+int btas_ewadd(int dtype, int kind, const void* a, const void* b, void* out, int64_t numel,
+               btas_stream_t stream);
+
+/* Tropical GEMM: C = (A (x) B) [(+) Z], with the reference's saturation
+ * semantics.  Replaces matmul/_product_tile/_saturation_limit
+ * (matrix.py:297-400).
+ *   integer_mode : the operands are integer-valued (reference `integer`
+ *                  flag); selects the integer saturation limit (2^53 f64,
+ *                  2^24 f32, always 2^28 for i32) and allows the S16X2 path.
+ *   Z, Cprev     : nullable.  Z is the accumulate_into operand (read only);
+ *                  Cprev sets BTAS_FLAG_CHANGED when C != Cprev bytewise.
+ *   C may alias Z but not A, B or Cprev.
+ * The kernel path is chosen ON THE DEVICE by an exact screen over per-k
+ * operand extremes, so the call never synchronises. */
+size_t btas_gemm_workspace_bytes(int dtype, int64_t M, int64_t N, int64_t K);
+int btas_gemm(int dtype, int kind, int integer_mode,
+              const void* A, int64_t lda, const void* B, int64_t ldb,
+              const void* Z, int64_t ldz, void* C, int64_t ldc,
+              int64_t M, int64_t N, int64_t K,
+              const void* Cprev, int64_t ldcp,
+              int32_t* dev_flags, void* workspace, size_t workspace_bytes,
+              btas_stream_t stream);
+
+/* Batched tropical matvec: Out[b, i] = (+)_k A[i, k] (x) V[b, k] for b < batch.
+ * Always masks overflow like matrix.py:403-425. */
+int btas_matvec(int dtype, int kind, int integer_mode,
+                const void* A, int64_t lda, int64_t M, int64_t K,
+                const void* V, int64_t ldv, int64_t batch,
+                void* Out, int64_t ldo, int32_t* dev_flags, btas_stream_t stream);
+
+/* Blocked three-phase Floyd-Warshall, in place on D (n x n, min-plus),
+ * bit-identical to the sequential k-round program of apsp.py:93-133
+ * (snapshot panels keep each round's operands exactly as the reference sees
+ * them).  `masked` selects the overflow-masking rounds (apsp.py:111-123) the
+ * reference uses when its screen fails; `max_abs`/`min_finite` are the scan of
+ * D used to choose the kernel path.  Sets BTAS_FLAG_SATURATED on masked
+ * overflow and BTAS_FLAG_DIAG_NEG when a diagonal entry ends < 0. */
+size_t btas_fw_workspace_bytes(int dtype, int64_t n);
+int btas_fw(int dtype, int integer_mode, void* D, int64_t ld, int64_t n, int masked,
+            double max_abs, double min_finite, int32_t* dev_flags,
+            void* workspace, size_t workspace_bytes, btas_stream_t stream);
+
+/* Diagonal test: sets BTAS_FLAG_DIAG_NEG if any d[i,i] < 0 (apsp.py:125,168). */
+int btas_diag_negative(int dtype, const void* d, int64_t ld, int64_t n, int32_t* dev_flags,
+                       btas_stream_t stream);
+
+/* Register/shared-memory microbenchmark of the add-min instruction mixes
+ * (the roofline denominator).  mix: 0 = f32 FADD2+FMNMX3, 1 = i32 VIADDMNMX,
+ * 2 = s16x2 VIADDMNMX.S16x2.  Writes pairs per SM clock and the effective
+ * SM clock (MHz) of the run.  Synchronises (diagnostic only). */
+int btas_probe_ceiling(int mix, double* pairs_per_clk_sm, double* sm_mhz, double* tpairs_per_s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BTAS_CUDA_H */

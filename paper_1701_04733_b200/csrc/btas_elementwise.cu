@@ -1,0 +1,523 @@
+// HBM-bound kernels of the hot path: ingest/validation, order-statistics
+// scans, fills, the closure base, elementwise ⊕ and the batched matvec.
+// All are grid-stride, 16-byte vectorised where alignment allows, and sized
+// to a multiple of the SM count.
+#include <algorithm>
+
+#include "btas_common.cuh"
+
+namespace btas {
+int device_sm_count();
+
+namespace {
+
+inline unsigned grid_for(int64_t work, int threads = 256) {
+  const int64_t blocks = ceil_div(work, threads);
+  const int64_t cap = (int64_t)device_sm_count() * 8;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, cap));
+}
+
+// ------------------------------------------------------------------ stats
+struct LocalStats {
+  unsigned long long nan = 0, neg_inf = 0, non_integral = 0, over = 0, out_of_range = 0, finite = 0;
+  double max_abs = -1.0;  // < 0: none
+  double mn = INFINITY, mx = -INFINITY;
+
+  BTAS_D void add_finite(double v, double int_limit) {
+    finite++;
+    if (v != floor(v)) non_integral++;
+    const double a = fabs(v);
+    if (a >= int_limit) over++;
+    max_abs = fmax(max_abs, a);
+    mn = fmin(mn, v);
+    mx = fmax(mx, v);
+  }
+};
+
+BTAS_D unsigned long long warp_sum(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+BTAS_D double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+BTAS_D double warp_min(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// warp-aggregated commit: one set of atomics per warp
+BTAS_D void commit(LocalStats s, btas_stats* out) {
+  s.nan = warp_sum(s.nan);
+  s.neg_inf = warp_sum(s.neg_inf);
+  s.non_integral = warp_sum(s.non_integral);
+  s.over = warp_sum(s.over);
+  s.out_of_range = warp_sum(s.out_of_range);
+  s.finite = warp_sum(s.finite);
+  s.max_abs = warp_max(s.max_abs);
+  s.mn = warp_min(s.mn);
+  s.mx = warp_max(s.mx);
+  if ((threadIdx.x & 31) != 0) return;
+  if (s.nan) atomicAdd(&out->nan_count, s.nan);
+  if (s.neg_inf) atomicAdd(&out->neg_inf_count, s.neg_inf);
+  if (s.non_integral) atomicAdd(&out->non_integral, s.non_integral);
+  if (s.over) atomicAdd(&out->over_limit, s.over);
+  if (s.out_of_range) atomicAdd(&out->out_of_range, s.out_of_range);
+  if (s.finite) {
+    atomicAdd(&out->finite_count, s.finite);
+    atomicMax(&out->max_abs_key, f64_key(s.max_abs));
+    atomicMin(&out->min_key, f64_key(s.mn));
+    atomicMax(&out->max_key, f64_key(s.mx));
+  }
+}
+
+__global__ void stats_init_kernel(btas_stats* s) {
+  s->nan_count = s->neg_inf_count = s->non_integral = s->over_limit = s->out_of_range = s->finite_count = 0;
+  s->max_abs_key = kKeyNone;
+  s->min_key = kKeyNoneMin;
+  s->max_key = kKeyNone;
+}
+
+// ------------------------------------------------------------------ ingest
+template <class S, class D>
+__global__ void ingest_kernel(bool min_plus, const S* __restrict__ src, int64_t n, D* __restrict__ dst,
+                              btas_stats* stats) {
+  LocalStats st;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double x = (double)src[i];
+    D out;
+    if (isnan(x)) {
+      st.nan++;
+      out = Traits<D>::eps(min_plus);
+    } else if (x == -INFINITY) {
+      st.neg_inf++;
+      out = Traits<D>::eps(min_plus);
+    } else if (x == INFINITY) {
+      out = Traits<D>::eps(min_plus);  // symbolic Infinity -> oriented (matrix.py:92-94)
+    } else {
+      const double v = x + 0.0;  // -0.0 -> +0.0 (matrix.py:92)
+      if constexpr (Traits<D>::dtype == BTAS_I32) {
+        if (v != floor(v) || fabs(v) >= (double)kI32Limit) {
+          st.out_of_range++;
+          out = 0;
+        } else {
+          out = (int32_t)v;
+        }
+        st.add_finite(v, Traits<D>::int_limit);
+      } else {
+        out = (D)v;
+        const double stored = (double)out;
+        if (isinf(stored)) {
+          st.out_of_range++;
+        } else {
+          st.add_finite(stored, Traits<D>::int_limit);
+        }
+      }
+    }
+    dst[i] = out;
+  }
+  commit(st, stats);
+}
+
+// ------------------------------------------------------------------ scan
+template <class T>
+__global__ void scan_kernel(const T* __restrict__ x, int64_t n, btas_stats* stats) {
+  LocalStats st;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const T v = x[i];
+    if constexpr (Traits<T>::dtype != BTAS_I32) {
+      if (isnan((double)v)) {
+        st.nan++;
+        continue;
+      }
+    }
+    if (Traits<T>::finite(v)) st.add_finite((double)v, Traits<T>::int_limit);
+  }
+  commit(st, stats);
+}
+
+template <class T>
+__global__ void to_f64_kernel(const T* __restrict__ x, int64_t n, double* __restrict__ y) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = Traits<T>::to_f64(x[i]);
+}
+
+template <class T>
+__global__ void fill_kernel(T* __restrict__ x, int64_t n, T v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = v;
+}
+
+template <class T>
+__global__ void identity_kernel(T* __restrict__ d, int64_t ld, int64_t n, T inf) {
+  const int64_t total = n * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n, j = e - i * n;
+    d[i * ld + j] = (i == j) ? (T)0 : inf;
+  }
+}
+
+template <class T>
+__global__ void closure_base_kernel(const T* __restrict__ s, int64_t lds, T* __restrict__ d, int64_t ldd, int64_t n) {
+  const int64_t total = n * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n, j = e - i * n;
+    T v = s[i * lds + j];
+    if (i == j && v > (T)0) v = (T)0;  // np.minimum(diag, 0.0) (apsp.py:88)
+    d[i * ldd + j] = v;
+  }
+}
+
+// elementwise ⊕, 16-byte vectors for the aligned body
+template <class T, bool MIN>
+__global__ void ewadd_kernel(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ o, int64_t n) {
+  constexpr int V = 16 / sizeof(T);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) |
+                         reinterpret_cast<uintptr_t>(o)) & 15) == 0;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t body = 0;
+  if (aligned) {
+    body = (n / V) * V;
+    const uint4* av = reinterpret_cast<const uint4*>(a);
+    const uint4* bv = reinterpret_cast<const uint4*>(b);
+    uint4* ov = reinterpret_cast<uint4*>(o);
+    for (int64_t i = tid; i < n / V; i += stride) {
+      uint4 x = av[i], y = bv[i], z;
+      const T* xs = reinterpret_cast<const T*>(&x);
+      const T* ys = reinterpret_cast<const T*>(&y);
+      T* zs = reinterpret_cast<T*>(&z);
+#pragma unroll
+      for (int v = 0; v < V; ++v) zs[v] = MIN ? (ys[v] < xs[v] ? ys[v] : xs[v]) : (ys[v] > xs[v] ? ys[v] : xs[v]);
+      ov[i] = z;
+    }
+  }
+  for (int64_t i = body + tid; i < n; i += stride) {
+    const T x = a[i], y = b[i];
+    o[i] = MIN ? (y < x ? y : x) : (y > x ? y : x);
+  }
+}
+
+template <class T>
+__global__ void diag_neg_kernel(const T* __restrict__ d, int64_t ld, int64_t n, int32_t* flags) {
+  bool neg = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    neg |= d[i * ld + i] < (T)0;
+  if (__any_sync(0xffffffffu, neg) && (threadIdx.x & 31) == 0) atomicOr(&flags[BTAS_FLAG_DIAG_NEG], 1);
+}
+
+// ------------------------------------------------------------------ matvec
+// Out[b, i] = ⊕_k A[i, k] ⊗ V[b, k].  R rows per CTA, NB vectors per pass.
+// The reference always masks overflow here (matrix.py:408-420): a finite ⊗
+// finite candidate that overflows (float) or reaches the integer limit
+// becomes ε and sets the flag.  HBM-bound, so the per-candidate test is free.
+template <class T, bool MIN>
+BTAS_D T mv_cand(T a, T v, bool int_mode, double limit, bool& sat) {
+  T s = a + v;
+  bool over;
+  if constexpr (Traits<T>::dtype == BTAS_I32) over = (s >= (T)kI32Limit) || (s <= -(T)kI32Limit);
+  else over = int_mode ? (fabs((double)s) >= limit) : isinf((double)s);
+  if (over && Traits<T>::finite(a) && Traits<T>::finite(v)) {
+    sat = true;
+    s = Traits<T>::eps(MIN);
+  }
+  return s;
+}
+
+template <class T, bool MIN, int R, int NB>
+__global__ void __launch_bounds__(256) matvec_kernel(const T* __restrict__ A, int64_t lda, int64_t M, int64_t K,
+                                                     const T* __restrict__ Vv, int64_t ldv, int nb,
+                                                     T* __restrict__ Out, int64_t ldo, int int_mode, double limit,
+                                                     int32_t* flags) {
+  constexpr int VEC = 16 / sizeof(T);
+  const int64_t r0 = (int64_t)blockIdx.x * R;
+  const T eps = Traits<T>::eps(MIN);
+  T acc[R][NB];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) acc[r][b] = eps;
+  bool sat = false;
+  const bool vec_ok = ((lda % VEC) == 0) && ((ldv % VEC) == 0) &&
+                      ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(Vv)) & 15) == 0;
+  const int64_t kvec_end = vec_ok ? (K / VEC) * VEC : 0;
+  for (int64_t k = (int64_t)threadIdx.x * VEC; k < kvec_end; k += (int64_t)blockDim.x * VEC) {
+    T vv[NB][VEC];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      if (b < nb) {
+        const uint4 u = *reinterpret_cast<const uint4*>(Vv + (int64_t)b * ldv + k);
+        const T* p = reinterpret_cast<const T*>(&u);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) vv[b][e] = p[e];
+      }
+    }
+    uint4 au[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int64_t row = r0 + r < M ? r0 + r : M - 1;
+      au[r] = __ldcs(reinterpret_cast<const uint4*>(A + row * lda + k));  // streamed once: evict-first
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const T* ap = reinterpret_cast<const T*>(&au[r]);
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        if (b < nb) {
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            const T s = mv_cand<T, MIN>(ap[e], vv[b][e], int_mode != 0, limit, sat);
+            acc[r][b] = MIN ? (s < acc[r][b] ? s : acc[r][b]) : (s > acc[r][b] ? s : acc[r][b]);
+          }
+        }
+      }
+    }
+  }
+  for (int64_t k = kvec_end + threadIdx.x; k < K; k += blockDim.x) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int64_t row = r0 + r < M ? r0 + r : M - 1;
+      const T a = A[row * lda + k];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        if (b < nb) {
+          const T s = mv_cand<T, MIN>(a, Vv[(int64_t)b * ldv + k], int_mode != 0, limit, sat);
+          acc[r][b] = MIN ? (s < acc[r][b] ? s : acc[r][b]) : (s > acc[r][b] ? s : acc[r][b]);
+        }
+      }
+    }
+  }
+  // block reduction of R*NB values
+  __shared__ T red[8][R * NB];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      T v = acc[r][b];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const T u = __shfl_xor_sync(0xffffffffu, v, o);
+        v = MIN ? (u < v ? u : v) : (u > v ? u : v);
+      }
+      if (l == 0) red[w][r * NB + b] = v;
+    }
+  __syncthreads();
+  if (threadIdx.x < R * NB) {
+    const int r = threadIdx.x / NB, b = threadIdx.x % NB;
+    T v = red[0][threadIdx.x];
+    for (int ww = 1; ww < (int)(blockDim.x >> 5); ++ww) {
+      const T u = red[ww][threadIdx.x];
+      v = MIN ? (u < v ? u : v) : (u > v ? u : v);
+    }
+    if constexpr (Traits<T>::dtype == BTAS_I32) {
+      if (MIN ? v >= (T)kI32Limit : v <= -(T)kI32Limit) v = eps;
+    }
+    if (r0 + r < M && b < nb) Out[(int64_t)b * ldo + r0 + r] = v;
+  }
+  if (__any_sync(0xffffffffu, sat) && l == 0) atomicOr(&flags[BTAS_FLAG_SATURATED], 1);
+}
+
+template <class T, bool MIN>
+int matvec_typed(int int_mode, const T* A, int64_t lda, int64_t M, int64_t K, const T* V, int64_t ldv,
+                 int64_t batch, T* Out, int64_t ldo, int32_t* flags, cudaStream_t st) {
+  const double limit = Traits<T>::dtype == BTAS_I32 ? (double)kI32Limit : Traits<T>::int_limit;
+  for (int64_t b0 = 0; b0 < batch; b0 += 8) {
+    const int nb = (int)std::min<int64_t>(8, batch - b0);
+    const T* Vb = V + b0 * ldv;
+    T* Ob = Out + b0 * ldo;
+    if (nb == 1) {
+      matvec_kernel<T, MIN, 16, 1><<<(unsigned)ceil_div(M, 16), 256, 0, st>>>(A, lda, M, K, Vb, ldv, nb, Ob, ldo,
+                                                                            int_mode, limit, flags);
+    } else if (nb <= 2) {
+      matvec_kernel<T, MIN, 8, 2><<<(unsigned)ceil_div(M, 8), 256, 0, st>>>(A, lda, M, K, Vb, ldv, nb, Ob, ldo,
+                                                                          int_mode, limit, flags);
+    } else if (nb <= 4) {
+      matvec_kernel<T, MIN, 8, 4><<<(unsigned)ceil_div(M, 8), 256, 0, st>>>(A, lda, M, K, Vb, ldv, nb, Ob, ldo,
+                                                                          int_mode, limit, flags);
+    } else {
+      matvec_kernel<T, MIN, 4, 8><<<(unsigned)ceil_div(M, 4), 256, 0, st>>>(A, lda, M, K, Vb, ldv, nb, Ob, ldo,
+                                                                          int_mode, limit, flags);
+    }
+    BTAS_CUDA_CHECK_LAUNCH();
+  }
+  return BTAS_OK;
+}
+
+inline bool valid_dtype(int d) { return d == BTAS_F32 || d == BTAS_I32 || d == BTAS_F64; }
+inline bool valid_kind(int k) { return k == BTAS_MIN_PLUS || k == BTAS_MAX_PLUS; }
+
+}  // namespace
+}  // namespace btas
+
+using namespace btas;
+
+#define BTAS_DISPATCH(dtype, ...)                          \
+  switch (dtype) {                                         \
+    case BTAS_F32: {                                       \
+      using T = float;                                     \
+      __VA_ARGS__;                                         \
+      break;                                               \
+    }                                                      \
+    case BTAS_I32: {                                       \
+      using T = int32_t;                                   \
+      __VA_ARGS__;                                         \
+      break;                                               \
+    }                                                      \
+    case BTAS_F64: {                                       \
+      using T = double;                                    \
+      __VA_ARGS__;                                         \
+      break;                                               \
+    }                                                      \
+    default:                                               \
+      return BTAS_ERR_INVALID;                             \
+  }
+
+extern "C" const char* btas_version(void) { return "btas-b200 0.1.0 (sm_100a)"; }
+
+extern "C" const char* btas_status_string(int status) {
+  switch (status) {
+    case BTAS_OK:
+      return "ok";
+    case BTAS_ERR_INVALID:
+      return "invalid argument";
+    case BTAS_ERR_CUDA: {
+      return "CUDA error";
+    }
+    case BTAS_ERR_WORKSPACE:
+      return "workspace too small";
+    case BTAS_ERR_UNSUPPORTED:
+      return "unsupported combination";
+    default:
+      return "unknown status";
+  }
+}
+
+extern "C" double btas_key_to_double(unsigned long long key) {
+  if (key == kKeyNone || key == kKeyNoneMin) return NAN;
+  return key_f64(key);
+}
+
+extern "C" int btas_stats_init(btas_stats* s, btas_stream_t stream) {
+  if (!s) return BTAS_ERR_INVALID;
+  stats_init_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(s);
+  BTAS_CUDA_CHECK_LAUNCH();
+  return BTAS_OK;
+}
+
+extern "C" int btas_ingest(int kind, int src_dtype, const void* src, int64_t numel, int dst_dtype, void* dst,
+                           btas_stats* stats, btas_stream_t stream) {
+  if (!src || !dst || !stats || numel < 0 || !valid_kind(kind) || !valid_dtype(dst_dtype)) return BTAS_ERR_INVALID;
+  if (src_dtype != BTAS_F64 && src_dtype != BTAS_F32) return BTAS_ERR_INVALID;
+  if (numel == 0) return BTAS_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool mn = kind == BTAS_MIN_PLUS;
+  const unsigned grid = grid_for(numel);
+  if (src_dtype == BTAS_F64) {
+    BTAS_DISPATCH(dst_dtype, ingest_kernel<double, T><<<grid, 256, 0, st>>>(mn, (const double*)src, numel, (T*)dst, stats))
+  } else {
+    BTAS_DISPATCH(dst_dtype, ingest_kernel<float, T><<<grid, 256, 0, st>>>(mn, (const float*)src, numel, (T*)dst, stats))
+  }
+  BTAS_CUDA_CHECK_LAUNCH();
+  return BTAS_OK;
+}
+
+extern "C" int btas_scan(int dtype, const void* x, int64_t numel, btas_stats* stats, btas_stream_t stream) {
+  if (!x || !stats || numel < 0) return BTAS_ERR_INVALID;
+  if (numel == 0) return BTAS_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  BTAS_DISPATCH(dtype, scan_kernel<T><<<grid_for(numel), 256, 0, st>>>((const T*)x, numel, stats))
+  BTAS_CUDA_CHECK_LAUNCH();
+  return BTAS_OK;
+}
+
+extern "C" int btas_to_f64(int dtype, const void* src, int64_t numel, double* dst, btas_stream_t stream) {
+  if (!src || !dst || numel < 0) return BTAS_ERR_INVALID;
+  if (numel == 0) return BTAS_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  BTAS_DISPATCH(dtype, to_f64_kernel<T><<<grid_for(numel), 256, 0, st>>>((const T*)src, numel, dst))
+  BTAS_CUDA_CHECK_LAUNCH();
+  return BTAS_OK;
+}
+
+extern "C" int btas_fill(int dtype, int kind, void* x, int64_t numel, double value, btas_stream_t stream) {
+  if (!x || numel < 0 || !valid_kind(kind) || isnan(value) || value == -INFINITY) return BTAS_ERR_INVALID;
+  if (numel == 0) return BTAS_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool mn = kind == BTAS_MIN_PLUS;
+  if (dtype == BTAS_I32 && !isinf(value) && (value != floor(value) || fabs(value) >= (double)kI32Limit))
+    return BTAS_ERR_INVALID;
+  BTAS_DISPATCH(dtype, {
+    const T v = isinf(value) ? Traits<T>::eps(mn) : (T)(value + 0.0);
+    fill_kernel<T><<<grid_for(numel), 256, 0, st>>>((T*)x, numel, v);
+  })
+  BTAS_CUDA_CHECK_LAUNCH();
+  return BTAS_OK;
+}
+
+extern "C" int btas_identity(int dtype, int kind, void* d, int64_t ld, int64_t n, btas_stream_t stream) {
+  if (!d || n < 0 || ld < n || !valid_kind(kind)) return BTAS_ERR_INVALID;
+  if (n == 0) return BTAS_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool mn = kind == BTAS_MIN_PLUS;
+  BTAS_DISPATCH(dtype, identity_kernel<T><<<grid_for(n * n), 256, 0, st>>>((T*)d, ld, n, Traits<T>::eps(mn)))
+  BTAS_CUDA_CHECK_LAUNCH();
+  return BTAS_OK;
+}
+
+extern "C" int btas_closure_base(int dtype, const void* src, int64_t lds, void* dst, int64_t ldd, int64_t n,
+                                 btas_stream_t stream) {
+  if (!src || !dst || n < 0 || lds < n || ldd < n) return BTAS_ERR_INVALID;
+  if (n == 0) return BTAS_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  BTAS_DISPATCH(dtype, closure_base_kernel<T><<<grid_for(n * n), 256, 0, st>>>((const T*)src, lds, (T*)dst, ldd, n))
+  BTAS_CUDA_CHECK_LAUNCH();
+  return BTAS_OK;
+}
+
+extern "C" int btas_ewadd(int dtype, int kind, const void* a, const void* b, void* out, int64_t numel,
+                          btas_stream_t stream) {
+  if (!a || !b || !out || numel < 0 || !valid_kind(kind)) return BTAS_ERR_INVALID;
+  if (numel == 0) return BTAS_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const unsigned grid = grid_for(ceil_div(numel, 4));
+  if (kind == BTAS_MIN_PLUS) {
+    BTAS_DISPATCH(dtype, ewadd_kernel<T, true><<<grid, 256, 0, st>>>((const T*)a, (const T*)b, (T*)out, numel))
+  } else {
+    BTAS_DISPATCH(dtype, ewadd_kernel<T, false><<<grid, 256, 0, st>>>((const T*)a, (const T*)b, (T*)out, numel))
+  }
+  BTAS_CUDA_CHECK_LAUNCH();
+  return BTAS_OK;
+}
+
+extern "C" int btas_diag_negative(int dtype, const void* d, int64_t ld, int64_t n, int32_t* flags,
+                                  btas_stream_t stream) {
+  if (!d || !flags || n < 0 || ld < n) return BTAS_ERR_INVALID;
+  if (n == 0) return BTAS_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  BTAS_DISPATCH(dtype, diag_neg_kernel<T><<<grid_for(n), 256, 0, st>>>((const T*)d, ld, n, flags))
+  BTAS_CUDA_CHECK_LAUNCH();
+  return BTAS_OK;
+}
+
+extern "C" int btas_matvec(int dtype, int kind, int integer_mode, const void* A, int64_t lda, int64_t M, int64_t K,
+                           const void* V, int64_t ldv, int64_t batch, void* Out, int64_t ldo, int32_t* flags,
+                           btas_stream_t stream) {
+  if (!A || !V || !Out || !flags || M < 1 || K < 1 || batch < 1 || lda < K || ldv < K || ldo < M ||
+      !valid_kind(kind))
+    return BTAS_ERR_INVALID;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool mn = kind == BTAS_MIN_PLUS;
+  int rc = BTAS_OK;
+  BTAS_DISPATCH(dtype, {
+    rc = mn ? matvec_typed<T, true>(integer_mode, (const T*)A, lda, M, K, (const T*)V, ldv, batch, (T*)Out, ldo,
+                                    flags, st)
+            : matvec_typed<T, false>(integer_mode, (const T*)A, lda, M, K, (const T*)V, ldv, batch, (T*)Out, ldo,
+                                     flags, st);
+  })
+  return rc;
+}

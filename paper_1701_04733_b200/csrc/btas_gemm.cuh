@@ -1,0 +1,432 @@
+// Tropical (min-plus / max-plus) GEMM core for sm_100a, shared by btas_gemm
+// (matmul, reference matrix.py:315-400) and the Floyd-Warshall phase-3 update
+// (btas_fw.cu).
+//
+// Design:
+//  * Operands are first packed into a k-pair-interleaved, tile-contiguous
+//    layout  P[blk][kp][r][2]  (blk = 32*G rows/cols, kp = k/2).  One pipeline
+//    stage of a tile is then ONE contiguous chunk, moved global->shared by a
+//    single bulk TMA copy (cp.async.bulk, SASS UBLKCP) completing on an
+//    mbarrier.  A producer warp keeps STAGES copies in flight; 8 consumer warps
+//    compute.  The kernel is persistent (one CTA per SM, static round-robin
+//    over output tiles in grouped raster order for L2 reuse).
+//  * Each consumer thread owns a (2*GM) x (2*GN) register microtile; rows
+//    ty*2 + 32*g + r, cols tx*2 + 32*h + c, so every shared-memory read is a
+//    conflict-free LDS.128 returning two rows (or cols) x one k pair.
+//  * Inner step per (i, j, k-pair) — the "mix" policies below:
+//      f32  : FADD2 {a_ik, a_ik+1} + {b_kj, b_k+1j}, then FMNMX3(acc, s.x, s.y)
+//      i32  : VIADDMNMX twice (DPX __viaddmin_s32 / __viaddmax_s32)
+//      s16x2: one 32-bit word holds the k and k+1 entries as int16 lanes;
+//             VIADDMNMX.S16x2 twice per word pair = 4 candidate pairs
+//      f64  : DADD + min
+//    min/max are exact and order-independent, every candidate is rounded
+//    once, so results are bit-identical to the reference's float64 ufuncs on
+//    the same inputs (matrix.py:9-13 determinism contract).
+//  * Epilogue fuses: integer-limit saturation clamp, the accumulate_into ⊕,
+//    the fixpoint compare against Cprev (apsp.py:161) and the diag<0 test.
+#pragma once
+
+#include "btas_common.cuh"
+
+namespace btas {
+
+constexpr int kConsumerWarps = 8;
+constexpr int kGemmThreads = (kConsumerWarps + 1) * 32;
+
+// ---------------------------------------------------------------------------
+// epilogue / kernel arguments
+// ---------------------------------------------------------------------------
+struct GemmArgs {
+  const void* Ap;        // packed A  [mblocks][Kp2][BM][2]
+  const void* Bp;        // packed B  [nblocks][Kp2][BN][2]
+  int64_t Kp2;           // k pairs in the packed layout (multiple of KP)
+  int64_t M, N;
+  int mblocks, nblocks;
+  const void* Z;         // nullable accumulate operand (storage dtype)
+  int64_t ldz;
+  void* C;
+  int64_t ldc;
+  const void* Cprev;     // nullable fixpoint reference
+  int64_t ldcp;
+  int32_t* flags;        // BTAS_NUM_FLAGS device ints
+  const int32_t* gate;   // nullable: run only when *gate == gate_value
+  int gate_value;
+  int64_t skip_lo, skip_hi;  // skip tiles whose rows or cols lie inside [lo, hi)
+  int integer_mode;
+  double limit;          // saturation limit (integer limit, or +inf for float mode)
+};
+
+// ---------------------------------------------------------------------------
+// inner-step policies
+// ---------------------------------------------------------------------------
+template <bool MIN>
+struct MixF32 {
+  using E = float;
+  using Acc = float;
+  using Out = float;
+  static constexpr int GM = 4, GN = 4, KP = 16, STAGES = 4;
+  static constexpr int path = BTAS_PATH_FAST32;
+  static constexpr bool kChecked = false;
+  BTAS_D static Acc init() { return MIN ? INFINITY : -INFINITY; }
+  BTAS_D static void step(Acc& c, E a0, E a1, E b0, E b1, bool&, const GemmArgs&) {
+    float2 s = __fadd2_rn(make_float2(a0, a1), make_float2(b0, b1));
+    c = MIN ? fminf(fminf(c, s.x), s.y) : fmaxf(fmaxf(c, s.x), s.y);
+  }
+  BTAS_D static Out finish(Acc c, const GemmArgs& a) {
+    // integer mode: sums at/after the float32 exactness limit saturate to Inf
+    // (the benign side; the other side is routed to the checked path)
+    if (a.integer_mode && (MIN ? (double)c >= a.limit : (double)c <= -a.limit)) c = MIN ? INFINITY : -INFINITY;
+    return c;
+  }
+};
+
+template <bool MIN>
+struct MixI32 {
+  using E = int32_t;
+  using Acc = int32_t;
+  using Out = int32_t;
+  static constexpr int GM = 4, GN = 4, KP = 16, STAGES = 4;
+  static constexpr int path = BTAS_PATH_FAST32;
+  static constexpr bool kChecked = false;
+  BTAS_D static Acc init() { return MIN ? kI32Inf : -kI32Inf; }
+  BTAS_D static void step(Acc& c, E a0, E a1, E b0, E b1, bool&, const GemmArgs&) {
+    if (MIN) {
+      c = __viaddmin_s32(a0, b0, c);
+      c = __viaddmin_s32(a1, b1, c);
+    } else {
+      c = __viaddmax_s32(a0, b0, c);
+      c = __viaddmax_s32(a1, b1, c);
+    }
+  }
+  BTAS_D static Out finish(Acc c, const GemmArgs&) {
+    // canonical Inf, and benign-side saturation at the int32 domain limit.
+    // The other side cannot be reached on this path (the screen routes it to
+    // CHECKED) except inside a negative cycle of Floyd-Warshall, where the
+    // clamp keeps int32 from wrapping so diag < 0 stays detectable.
+    if (MIN) return c >= kI32Limit ? kI32Inf : (c < -kI32Limit ? -kI32Limit : c);
+    return c <= -kI32Limit ? -kI32Inf : (c > kI32Limit ? kI32Limit : c);
+  }
+};
+
+template <bool MIN>
+struct MixF64 {
+  using E = double;
+  using Acc = double;
+  using Out = double;
+  static constexpr int GM = 2, GN = 4, KP = 16, STAGES = 3;
+  static constexpr int path = BTAS_PATH_FAST64;
+  static constexpr bool kChecked = false;
+  BTAS_D static Acc init() { return MIN ? INFINITY : -INFINITY; }
+  BTAS_D static void step(Acc& c, E a0, E a1, E b0, E b1, bool&, const GemmArgs&) {
+    double s0 = __dadd_rn(a0, b0), s1 = __dadd_rn(a1, b1);
+    c = MIN ? fmin(fmin(c, s0), s1) : fmax(fmax(c, s0), s1);
+  }
+  BTAS_D static Out finish(Acc c, const GemmArgs& a) {
+    if (a.integer_mode && (MIN ? c >= a.limit : c <= -a.limit)) c = MIN ? INFINITY : -INFINITY;
+    return c;
+  }
+};
+
+// int16x2 lanes: E is a word holding (k even, k odd) entries; acc lanes hold
+// the running ⊕ of even-k and odd-k candidates, merged in finish().
+template <bool MIN, class OutT>
+struct MixS16 {
+  using E = uint32_t;
+  using Acc = uint32_t;
+  using Out = OutT;
+  static constexpr int GM = 4, GN = 4, KP = 16, STAGES = 4;
+  static constexpr int path = BTAS_PATH_S16X2;
+  static constexpr bool kChecked = false;
+  BTAS_D static Acc init() {
+    const uint32_t inf = MIN ? (uint32_t)kS16Inf : (uint32_t)(uint16_t)(-kS16Inf);
+    return inf | (inf << 16);
+  }
+  BTAS_D static void step(Acc& c, E a0, E a1, E b0, E b1, bool&, const GemmArgs&) {
+    if (MIN) {
+      c = __viaddmin_s16x2(a0, b0, c);
+      c = __viaddmin_s16x2(a1, b1, c);
+    } else {
+      c = __viaddmax_s16x2(a0, b0, c);
+      c = __viaddmax_s16x2(a1, b1, c);
+    }
+  }
+  BTAS_D static Out finish(Acc c, const GemmArgs&) {
+    int lo = (int)(int16_t)(c & 0xFFFFu);
+    int hi = (int)(int16_t)(c >> 16);
+    int r = MIN ? min(lo, hi) : max(lo, hi);
+    if (MIN ? r >= kS16InfThreshold : r <= -kS16InfThreshold) return Traits<OutT>::eps(MIN);
+    return (OutT)r;
+  }
+};
+
+// Per-candidate overflow masking: the reference's masked tile
+// (matrix.py:334-342): a finite (x) finite sum that overflows (float) or
+// reaches the integer limit (integer mode) becomes ε and raises the flag.
+template <class T, bool MIN>
+struct MixChecked {
+  using E = T;
+  using Acc = T;
+  using Out = T;
+  static constexpr int GM = sizeof(T) == 8 ? 2 : 4, GN = 4, KP = 16, STAGES = sizeof(T) == 8 ? 3 : 4;
+  static constexpr int path = BTAS_PATH_CHECKED;
+  static constexpr bool kChecked = true;
+  BTAS_D static Acc init() { return Traits<T>::eps(MIN); }
+  BTAS_D static T cand(T a, T b, bool& sat, const GemmArgs& g) {
+    T s = a + b;
+    bool over;
+    if (sizeof(T) == 4 && Traits<T>::dtype == BTAS_I32) {
+      over = (s >= (T)kI32Limit) || (s <= -(T)kI32Limit);
+    } else if (g.integer_mode) {
+      over = fabs((double)s) >= g.limit;
+    } else {
+      over = isinf((double)s);
+    }
+    if (over && Traits<T>::finite(a) && Traits<T>::finite(b)) {
+      sat = true;
+      s = Traits<T>::eps(MIN);
+    }
+    return s;
+  }
+  BTAS_D static void step(Acc& c, E a0, E a1, E b0, E b1, bool& sat, const GemmArgs& g) {
+    T s0 = cand(a0, b0, sat, g), s1 = cand(a1, b1, sat, g);
+    if (MIN) {
+      c = s0 < c ? s0 : c;
+      c = s1 < c ? s1 : c;
+    } else {
+      c = s0 > c ? s0 : c;
+      c = s1 > c ? s1 : c;
+    }
+  }
+  BTAS_D static Out finish(Acc c, const GemmArgs&) {
+    if (Traits<T>::dtype == BTAS_I32) {
+      if (MIN) return c >= (T)kI32Limit ? (T)kI32Inf : c;
+      return c <= -(T)kI32Limit ? (T)(-kI32Inf) : c;
+    }
+    return c;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// helpers
+// ---------------------------------------------------------------------------
+template <class E>
+BTAS_D void lds4(const E* p, E out[4]) {
+  if constexpr (sizeof(E) == 4) {
+    uint4 v = *reinterpret_cast<const uint4*>(p);
+    out[0] = __builtin_bit_cast(E, v.x);
+    out[1] = __builtin_bit_cast(E, v.y);
+    out[2] = __builtin_bit_cast(E, v.z);
+    out[3] = __builtin_bit_cast(E, v.w);
+  } else {
+    double2 v0 = reinterpret_cast<const double2*>(p)[0];
+    double2 v1 = reinterpret_cast<const double2*>(p)[1];
+    out[0] = v0.x;
+    out[1] = v0.y;
+    out[2] = v1.x;
+    out[3] = v1.y;
+  }
+}
+
+template <class T>
+BTAS_D bool bits_differ(T a, T b) {
+  if constexpr (sizeof(T) == 4) return __builtin_bit_cast(uint32_t, a) != __builtin_bit_cast(uint32_t, b);
+  else return __builtin_bit_cast(unsigned long long, a) != __builtin_bit_cast(unsigned long long, b);
+}
+
+template <class T, bool MIN>
+BTAS_D T combine(T a, T b) {
+  if (MIN) return b < a ? b : a;
+  return b > a ? b : a;
+}
+
+BTAS_D void tile_coords(int tile, int mblocks, int nblocks, int& mb, int& nb) {
+  constexpr int kGroup = 8;
+  const int per_group = kGroup * nblocks;
+  const int gid = tile / per_group;
+  const int first = gid * kGroup;
+  const int gsz = min(mblocks - first, kGroup);
+  const int in = tile - gid * per_group;
+  mb = first + in % gsz;
+  nb = in / gsz;
+}
+
+template <class P>
+struct GemmShape {
+  static constexpr int BM = 32 * P::GM;
+  static constexpr int BN = 32 * P::GN;
+  static constexpr int A_ELEMS = P::KP * BM * 2;
+  static constexpr int B_ELEMS = P::KP * BN * 2;
+  static constexpr size_t smem_bytes =
+      (size_t)P::STAGES * (A_ELEMS + B_ELEMS) * sizeof(typename P::E) + 2 * P::STAGES * sizeof(uint64_t);
+};
+
+// ---------------------------------------------------------------------------
+// the kernel
+// ---------------------------------------------------------------------------
+template <class P, bool MIN>
+__global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __grid_constant__ GemmArgs g) {
+  if (g.gate != nullptr && *g.gate != g.gate_value) return;
+  using E = typename P::E;
+  using Acc = typename P::Acc;
+  using Out = typename P::Out;
+  using S = GemmShape<P>;
+  constexpr int GM = P::GM, GN = P::GN, KP = P::KP, ST = P::STAGES;
+  constexpr int BM = S::BM, BN = S::BN;
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  E* sA = reinterpret_cast<E*>(smem_raw);
+  E* sB = sA + ST * S::A_ELEMS;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + ST * S::B_ELEMS);
+  uint64_t* empty = full + ST;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const int ntiles = g.mblocks * g.nblocks;
+  const int nkb = (int)(g.Kp2 / KP);
+
+  auto skipped = [&](int mb, int nb) {
+    if (g.skip_hi <= g.skip_lo) return false;
+    const int64_t r0 = (int64_t)mb * BM, c0 = (int64_t)nb * BN;
+    return (r0 >= g.skip_lo && r0 + BM <= g.skip_hi) || (c0 >= g.skip_lo && c0 + BN <= g.skip_hi);
+  };
+
+  if (warp == kConsumerWarps) {
+    // ------------------------------ producer ------------------------------
+    if (lane == 0) {
+      const E* Ap = static_cast<const E*>(g.Ap);
+      const E* Bp = static_cast<const E*>(g.Bp);
+      uint32_t it = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        int mb, nb;
+        tile_coords(tile, g.mblocks, g.nblocks, mb, nb);
+        if (skipped(mb, nb)) continue;
+        const E* gA = Ap + (size_t)mb * g.Kp2 * BM * 2;
+        const E* gB = Bp + (size_t)nb * g.Kp2 * BN * 2;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % ST;
+          if (it >= (uint32_t)ST) mbar_wait(&empty[s], ((it / ST) - 1) & 1);
+          mbar_arrive_expect_tx(&full[s], (uint32_t)((S::A_ELEMS + S::B_ELEMS) * sizeof(E)));
+          bulk_g2s(sA + s * S::A_ELEMS, gA + (size_t)kb * S::A_ELEMS, S::A_ELEMS * sizeof(E), &full[s]);
+          bulk_g2s(sB + s * S::B_ELEMS, gB + (size_t)kb * S::B_ELEMS, S::B_ELEMS * sizeof(E), &full[s]);
+        }
+      }
+    }
+    return;
+  }
+
+  // ------------------------------ consumers -------------------------------
+  const int ty = (warp >> 1) * 4 + (lane >> 3);  // 0..15
+  const int tx = (warp & 1) * 8 + (lane & 7);    // 0..15
+  bool changed = false, diag_neg = false, sat = false;
+  uint32_t it = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    int mb, nb;
+    tile_coords(tile, g.mblocks, g.nblocks, mb, nb);
+    if (skipped(mb, nb)) continue;
+
+    Acc acc[GM][2][GN][2];
+#pragma unroll
+    for (int i = 0; i < GM; ++i)
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int j = 0; j < GN; ++j)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) acc[i][r][j][c] = P::init();
+
+    for (int kb = 0; kb < nkb; ++kb, ++it) {
+      const int s = it % ST;
+      mbar_wait(&full[s], (it / ST) & 1);
+      const E* tA = sA + s * S::A_ELEMS + ty * 4;
+      const E* tB = sB + s * S::B_ELEMS + tx * 4;
+#pragma unroll 2
+      for (int kp = 0; kp < KP; ++kp) {
+        E a[GM][4], b[GN][4];
+#pragma unroll
+        for (int i = 0; i < GM; ++i) lds4(tA + kp * BM * 2 + i * 64, a[i]);
+#pragma unroll
+        for (int j = 0; j < GN; ++j) lds4(tB + kp * BN * 2 + j * 64, b[j]);
+#pragma unroll
+        for (int i = 0; i < GM; ++i)
+#pragma unroll
+          for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int j = 0; j < GN; ++j)
+#pragma unroll
+              for (int c = 0; c < 2; ++c)
+                P::step(acc[i][r][j][c], a[i][2 * r], a[i][2 * r + 1], b[j][2 * c], b[j][2 * c + 1], sat, g);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+
+    // ------------------------------ epilogue ------------------------------
+    Out* C = static_cast<Out*>(g.C);
+    const Out* Z = static_cast<const Out*>(g.Z);
+    const Out* Cp = static_cast<const Out*>(g.Cprev);
+#pragma unroll
+    for (int i = 0; i < GM; ++i)
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int64_t row = (int64_t)mb * BM + i * 32 + ty * 2 + r;
+        if (row >= g.M) continue;
+#pragma unroll
+        for (int j = 0; j < GN; ++j)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const int64_t col = (int64_t)nb * BN + j * 32 + tx * 2 + c;
+            if (col >= g.N) continue;
+            Out v = P::finish(acc[i][r][j][c], g);
+            if (Z != nullptr) v = combine<Out, MIN>(v, Z[row * g.ldz + col]);
+            if (Cp != nullptr) changed |= bits_differ(v, Cp[row * g.ldcp + col]);
+            if (row == col) diag_neg |= (v < (Out)0);
+            C[row * g.ldc + col] = v;
+          }
+      }
+  }
+  if (__any_sync(0xffffffffu, changed) && lane == 0) atomicOr(&g.flags[BTAS_FLAG_CHANGED], 1);
+  if (__any_sync(0xffffffffu, diag_neg) && lane == 0) atomicOr(&g.flags[BTAS_FLAG_DIAG_NEG], 1);
+  if (P::kChecked) {
+    if (__any_sync(0xffffffffu, sat) && lane == 0) atomicOr(&g.flags[BTAS_FLAG_SATURATED], 1);
+  }
+}
+
+// host-side launcher for one policy
+int device_sm_count();
+
+template <class P, bool MIN>
+int launch_tropical_gemm(const GemmArgs& g, cudaStream_t stream) {
+  using S = GemmShape<P>;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(tropical_gemm_kernel<P, MIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)S::smem_bytes) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return BTAS_ERR_CUDA;
+    }
+    configured = true;
+  }
+  const int ntiles = g.mblocks * g.nblocks;
+  const int grid = ntiles < device_sm_count() ? ntiles : device_sm_count();
+  if (grid <= 0) return BTAS_OK;
+  tropical_gemm_kernel<P, MIN><<<grid, kGemmThreads, S::smem_bytes, stream>>>(g);
+  BTAS_CUDA_CHECK_LAUNCH();
+  return BTAS_OK;
+}
+
+// packed-layout index: P[blk][kp][r][2]
+BTAS_HD int64_t packed_index(int64_t rc, int64_t k, int64_t Kp2, int BLK) {
+  const int64_t blk = rc / BLK, r = rc - blk * BLK;
+  return ((blk * Kp2 + (k >> 1)) * BLK + r) * 2 + (k & 1);
+}
+
+}  // namespace btas
