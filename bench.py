@@ -1,0 +1,491 @@
+#!/usr/bin/env python3
+"""Benchmark of the tropical hot path on B200 (driver contract: one JSON line).
+
+Default workload (BASELINE.json configs[1]): min-plus GEMM, n = 16384, int32
+storage ("DPX"), operands uniform integers in [-1000, 1000] with 25 % Infinity
+(the C2 recipe of SURVEY §8(d)).  One step = one C = A ⊗ B through the
+product path (btas_gemm: screen, packing, GEMM kernel) with A, B resident in
+HBM.  Metric: G(add,min)/s = n^3 / step time / 1e9.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+                    [--workload gemm|gemm_f32|gemm_f32_real|fw|apsp] [--n N]
+
+N > 1 (launched by torchrun, one rank per GPU): every rank runs its own
+independent GEMM of the same size — the GEMM shards into independent output
+blocks, there is no data-path collective (weak scaling); the elapsed time is
+the max over ranks.
+
+Keys beyond the base contract:
+  roofline      the GEMM kernel's achieved pair rate (CUDA events around the
+                kernel launches, on the launching stream) vs the live ceiling
+                of its instruction mix (btas_probe_ceiling: pairs/clk/SM x SMs
+                x the SM clock sampled during the timed region)
+  cpu_baseline  the reference algorithm restated in NumPy (oracle/tropical.py,
+                "port": the reference's broadcast-add + reduce tiles on a
+                thread pool), timed on this host on a sampled row block
+  e2e           the same metric through the public API from pinned host
+                buffers: TropicalMatrix(host) x2 + matmul + D2H of the result
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "tropical GEMM G(add,min)/s at n=16384"
+UNIT = "Gpair/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[1])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="gemm", choices=["gemm", "gemm_f32", "gemm_f32_real", "fw", "apsp"])
+    ap.add_argument("--n", type=int, default=0, help="problem size (default per workload)")
+    ap.add_argument("--no-variants", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region (B200_PROFILING.md clocks line)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# synthetic inputs
+# ---------------------------------------------------------------------------
+def gemm_inputs(n, dtype, device, seed, real=False):
+    """C2 recipe: integers in [-1000, 1000] (or reals rounded to f32), 25 % Infinity."""
+    import torch
+
+    import paper_1701_04733_b200 as bt
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    if real:
+        sym = (torch.rand((n, n), generator=g, device=device, dtype=torch.float32) * 2000.0 - 1000.0)
+    else:
+        sym = torch.randint(-1000, 1001, (n, n), generator=g, device=device, dtype=torch.int32).to(torch.float32)
+    inf_mask = torch.rand((n, n), generator=g, device=device) < 0.25
+    sym[inf_mask] = math.inf
+    m = bt.TropicalMatrix(bt.SemiringKind.MIN_PLUS, sym, dtype=dtype, device=device)
+    return m, sym
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference algorithm (NumPy port), sampled rows
+# ---------------------------------------------------------------------------
+def cpu_baseline_gemm(x_sym_rows, y_sym, storage, integer, budget_rows):
+    from oracle import tropical as ot
+
+    cores = len(os.sched_getaffinity(0))
+    xo = ot.orient(ot.MIN, x_sym_rows[:budget_rows])
+    yo = ot.orient(ot.MIN, y_sym)
+    ot.matmul(xo[:1], yo[:, :256], ot.MIN, storage, integer)  # warm-up
+    t = time.perf_counter()
+    ot.matmul(xo, yo, ot.MIN, storage, integer, tile_rows=4, tile_cols=128, workers=cores)
+    dt = time.perf_counter() - t
+    pairs = xo.shape[0] * yo.shape[0] * yo.shape[1]
+    return pairs / dt / 1e9, cores, dt, pairs
+
+
+def cpu_sample_rows():
+    cores = len(os.sched_getaffinity(0))
+    return int(min(256, max(8, 4 * cores)))
+
+
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    if args.workload in ("fw", "apsp"):
+        return apsp_arm(args, rank, world, dev)
+
+    import paper_1701_04733_b200 as bt
+    from paper_1701_04733_b200 import _lib
+
+    n = args.n or 16384
+    dtype, real, wl = {
+        "gemm": (torch.int32, False, f"minplus_gemm_n{n}_i32"),
+        "gemm_f32": (torch.float32, False, f"minplus_gemm_n{n}_f32_integer"),
+        "gemm_f32_real": (torch.float32, True, f"minplus_gemm_n{n}_f32_real"),
+    }[args.workload]
+
+    # ------------------------------------------------------------- timed run
+    from paper_1701_04733_b200 import matrix as bm
+
+    seed = 0xB2000001 + 7919 * rank
+    x, xs = gemm_inputs(n, dtype, dev, seed, real)
+    y, ys = gemm_inputs(n, dtype, dev, seed + 1, real)
+    integer = x.integer and y.integer
+    out = torch.empty((n, n), dtype=dtype, device=dev)
+    flags = None
+    for _ in range(max(3, args.warmup)):
+        _, flags = bm._gemm(x.data, y.data, bt.SemiringKind.MIN_PLUS, integer, out=out)
+    torch.cuda.synchronize()
+    path_bits = int(flags[_lib.FLAG_PATH].item())
+    path = [name for p, name in _lib.PATH_NAMES.items() if path_bits & (1 << p)][0]
+
+    stream = torch.cuda.current_stream(dev)
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    _lib.gemm_timing(True)
+    with ClockSampler(local) as clocks:
+        start.record(stream)
+        for _ in range(args.steps):
+            bm._gemm(x.data, y.data, bt.SemiringKind.MIN_PLUS, integer, out=out)
+        stop.record(stream)
+        torch.cuda.synchronize()
+    kernel_ms, kernel_count = _lib.gemm_timing_read()
+    _lib.gemm_timing(False)
+    elapsed_ms = start.elapsed_time(stop)
+    if world > 1:
+        t = torch.tensor([elapsed_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+        dist.barrier()
+    pairs = float(n) ** 3
+    value = pairs * args.steps * world / (elapsed_ms * 1e-3) / 1e9
+    clk = clocks.summary()
+
+    # roofline: the GEMM kernel vs the live ceiling of its instruction mix
+    mix = {"s16x2": 2, "fast32": 1 if dtype == torch.int32 else 0}.get(path, 0)
+    probe = _lib.probe_ceiling(mix)
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    sm_mhz = clk["sm_mhz"] or probe["sm_mhz"]
+    peak = probe["pairs_per_clk_sm"] * nsm * sm_mhz * 1e6 / 1e12
+    achieved = pairs / (kernel_ms / kernel_count * 1e-3) / 1e12
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get(wl)
+    roofline = {
+        "bound": "alu",
+        "achieved": round(achieved, 3),
+        "peak": round(peak, 3),
+        "unit": "Tpair/s",
+        "frac": round(achieved / peak, 4),
+        "traffic": traffic,
+        "kernel": {"s16x2": "tropical_gemm_kernel<MixS16>", "fast32": "tropical_gemm_kernel<MixI32|MixF32>"}.get(
+            path, path),
+        "kernel_ms": round(kernel_ms / kernel_count, 3),
+        "step_ms": round(elapsed_ms / args.steps, 3),
+        "peak_mix_pairs_per_clk_sm": round(probe["pairs_per_clk_sm"], 2),
+        "peak_sm_mhz": sm_mhz,
+        "peak_source": "btas_probe_ceiling (live register/LDS microbenchmark of the same add-min instruction mix) "
+                       "x SMs x median SM clock during the timed region",
+        "peak_at_max_clock": round(probe["pairs_per_clk_sm"] * nsm * 1965e6 / 1e12, 3),
+    }
+
+    result = {
+        "metric": METRIC,
+        "value": round(value, 1),
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": max(3, args.warmup),
+        "ms_per_step": round(elapsed_ms / args.steps, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": {torch.int32: "i32", torch.float32: "f32"}[dtype],
+        "data": "synthetic",
+        "config": {
+            "workload": wl,
+            "n": n,
+            "operands": "uniform reals in [-1000,1000) rounded to f32" if real else "uniform integers in [-1000,1000]",
+            "infinity_fraction": 0.25,
+            "kernel_path": path,
+            "l2": "operands 1 GiB each >> 126 MB L2; no flush needed",
+            "parallelism": f"dp{world} (independent GEMM per GPU)",
+        },
+        "roofline": roofline,
+        "gpu_launches": args.steps * (11 if integer else 8),
+        "clocks": clk,
+    }
+
+    # ------------------------------------------------------------- e2e (public API, host buffers)
+    if not args.no_e2e:
+        result["e2e"] = e2e_gemm(n, dtype, xs, ys, dev, steps=min(args.steps, 3))
+
+    # ------------------------------------------------------------- other kernel paths
+    if not args.no_variants and args.workload == "gemm":
+        result["variants"] = variants(n, dev, rank)
+
+    # ------------------------------------------------------------- CPU baseline (rank 0, N = 1)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rows = cpu_sample_rows()
+        storage = {torch.int32: "i32", torch.float32: "f32"}[dtype]
+        xh = xs[:rows].double().cpu().numpy()
+        yh = ys.double().cpu().numpy()
+        v, cores, secs, spairs = cpu_baseline_gemm(xh, yh, storage, integer, rows)
+        result["cpu_baseline"] = {
+            "value": round(v, 4), "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{rows} rows x {n} x {n} ({spairs:.3g} pairs, {secs:.1f} s) of the same operands; "
+                      "NumPy restatement of btas.matmul (_product_tile broadcast-add + reduce, thread pool of "
+                      f"{cores} workers)",
+        }
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def e2e_gemm(n, dtype, xs, ys, dev, steps):
+    """Public API end to end: host symbolic operands (pinned f32) -> two
+    TropicalMatrix constructions (H2D + validation/ingest) -> matmul -> D2H of
+    the result storage into pinned memory."""
+    import torch
+
+    import paper_1701_04733_b200 as bt
+
+    hx = xs.cpu().pin_memory()
+    hy = ys.cpu().pin_memory()
+    hout = torch.empty((n, n), dtype=dtype).pin_memory()
+    MIN = bt.SemiringKind.MIN_PLUS
+
+    def step():
+        X = bt.TropicalMatrix(MIN, hx, dtype=dtype, device=dev)
+        Y = bt.TropicalMatrix(MIN, hy, dtype=dtype, device=dev)
+        Z = bt.matmul(X, Y)
+        hout.copy_(Z.data, non_blocking=True)
+        torch.cuda.synchronize()
+
+    step()
+    t = time.perf_counter()
+    for _ in range(steps):
+        step()
+    dt = (time.perf_counter() - t) / steps
+    return {
+        "value": round(float(n) ** 3 / dt / 1e9, 1),
+        "unit": UNIT,
+        "h2d_bytes_per_step": 2 * n * n * 4,
+        "d2h_bytes_per_step": n * n * torch.tensor([], dtype=dtype).element_size(),
+        "ms_per_step": round(dt * 1e3, 2),
+        "steps": steps,
+        "path": "TropicalMatrix(host pinned f32) x2 -> matmul -> result D2H (pinned)",
+    }
+
+
+def variants(n, dev, rank):
+    """The other kernel paths on the same size (fewer steps)."""
+    import torch
+
+    import paper_1701_04733_b200 as bt
+    from paper_1701_04733_b200 import _lib
+    from paper_1701_04733_b200 import matrix as bm
+
+    out = {}
+    cases = {
+        "f32_integer_valued": (torch.float32, False, 1000),
+        "f32_real_valued": (torch.float32, True, 1000),
+        "i32_wide_range": (torch.int32, False, 10**6),
+    }
+    for name, (dtype, real, rng) in cases.items():
+        g = torch.Generator(device=dev)
+        g.manual_seed(0xB2000002 + rank)
+        mats = []
+        for _ in range(2):
+            if real:
+                sym = torch.rand((n, n), generator=g, device=dev) * 2000.0 - 1000.0
+            else:
+                sym = torch.randint(-rng, rng + 1, (n, n), generator=g, device=dev, dtype=torch.int32).to(torch.float32)
+            sym[torch.rand((n, n), generator=g, device=dev) < 0.25] = math.inf
+            mats.append(bt.TropicalMatrix(bt.SemiringKind.MIN_PLUS, sym, dtype=dtype, device=dev))
+            del sym
+        x, y = mats
+        integer = x.integer and y.integer
+        o = torch.empty((n, n), dtype=dtype, device=dev)
+        _, flags = bm._gemm(x.data, y.data, bt.SemiringKind.MIN_PLUS, integer, out=o)
+        torch.cuda.synchronize()
+        bits = int(flags[_lib.FLAG_PATH].item())
+        path = [nm for p, nm in _lib.PATH_NAMES.items() if bits & (1 << p)][0]
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        _lib.gemm_timing(True)
+        s.record()
+        for _ in range(3):
+            bm._gemm(x.data, y.data, bt.SemiringKind.MIN_PLUS, integer, out=o)
+        e.record()
+        torch.cuda.synchronize()
+        kms, kc = _lib.gemm_timing_read()
+        _lib.gemm_timing(False)
+        ms = s.elapsed_time(e) / 3
+        mix = {"s16x2": 2}.get(path, 1 if dtype == torch.int32 else 0)
+        probe = _lib.probe_ceiling(mix)
+        nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+        peak = probe["pairs_per_clk_sm"] * nsm * probe["sm_mhz"] * 1e6 / 1e12
+        ach = float(n) ** 3 / (kms / kc * 1e-3) / 1e12
+        out[name] = {"value": round(float(n) ** 3 / (ms * 1e-3) / 1e9, 1), "unit": UNIT, "kernel_path": path,
+                     "kernel_tpairs": round(ach, 3), "peak_tpairs_probe_clock": round(peak, 3),
+                     "frac": round(ach / peak, 4)}
+        del x, y, o, mats
+        torch.cuda.empty_cache()
+    return out
+
+
+def apsp_arm(args, rank, world, dev):
+    """FW (C3) / squaring (C1, C4) timing on one GPU (replicas for N > 1)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1701_04733_b200 as bt
+    from paper_1701_04733_b200.graphs import instance_seed, random_graph_matrix
+
+    n = args.n or (32768 if args.workload == "fw" else 512)
+    dtype = torch.int32 if args.workload == "fw" else torch.float32
+    adj = random_graph_matrix(n, 0.5, (1, 100), instance_seed(1, n), dtype=dtype, device=dev)
+    solver = bt.floyd_warshall if args.workload == "fw" else bt.apsp_by_squaring
+    for _ in range(max(1, min(args.warmup, 3))):
+        rep = solver(adj)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t = time.perf_counter()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(args.steps):
+        rep = solver(adj)
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / args.steps
+    mults = rep.multiplications_performed
+    pairs = float(n) ** 3 * (1 if args.workload == "fw" else mults)
+    res = {"metric": f"APSP time n={n}", "value": round(ms / 1e3, 4), "unit": "s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False,
+           "scaling": "weak", "vs_baseline": None, "dtype": "i32" if dtype == torch.int32 else "f32",
+           "data": "synthetic",
+           "config": {"workload": f"{args.workload}_n{n}", "graph": "random_graph p=0.5 weights 1..100",
+                      "multiplications": mults, "negative_cycle": rep.negative_cycle,
+                      "gpairs_per_s": round(pairs / (ms * 1e-3) / 1e9, 1)}}
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    return 0
+
+
+def reference_arm(args, rank, world):
+    """The reference's own CPU algorithm (NumPy port of btas.matmul, every
+    host thread) on a bounded sample of the same workload; rank 0 only."""
+    if rank != 0:
+        return 0
+    import numpy as np
+
+    from oracle import tropical as ot
+
+    n = args.n or 16384
+    rng = np.random.default_rng(0xB2000001)
+    rows = cpu_sample_rows()
+    xs = rng.integers(-1000, 1001, (rows, n)).astype(np.float64)
+    xs[rng.random((rows, n)) < 0.25] = math.inf
+    ys = rng.integers(-1000, 1001, (n, n)).astype(np.float64)
+    ys[rng.random((n, n)) < 0.25] = math.inf
+    xo, yo = ot.orient(ot.MIN, xs), ot.orient(ot.MIN, ys)
+    cores = len(os.sched_getaffinity(0))
+    times = []
+    for i in range(args.warmup + args.steps):
+        t = time.perf_counter()
+        ot.matmul(xo, yo, ot.MIN, "i32", True, tile_rows=4, tile_cols=128, workers=cores)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t)
+    pairs = rows * n * n
+    value = pairs / statistics.median(times) / 1e9
+    res = {
+        "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(statistics.median(times) * 1e3, 1), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "i32", "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"minplus_gemm_n{n}_i32", "n": n,
+                   "sample": f"{rows} rows x {n} x {n} per step", "operands": "uniform integers in [-1000,1000]",
+                   "infinity_fraction": 0.25},
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{rows} rows x {n} x {n} per step (NumPy restatement of btas.matmul, "
+                                   f"thread pool of {cores})"},
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(res), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    raise SystemExit(main())

@@ -142,6 +142,13 @@ int btas_gemm(int dtype, int kind, int integer_mode,
               int32_t* dev_flags, void* workspace, size_t workspace_bytes,
               btas_stream_t stream);
 
+/* Measurement hooks (bench.py): when enabled, every btas_gemm brackets its
+ * GEMM kernel launches (not the screen/packing) with CUDA events recorded on
+ * the caller's stream; btas_gemm_timing_read synchronises on them and returns
+ * the summed kernel time and the number of bracketed calls (then clears). */
+int btas_gemm_timing(int enable);
+int btas_gemm_timing_read(double* total_ms, int* count);
+
 /* Batched tropical matvec: Out[b, i] = (+)_k A[i, k] (x) V[b, k] for b < batch.
  * Always masks overflow like matrix.py:403-425. */
 int btas_matvec(int dtype, int kind, int integer_mode,

@@ -57,13 +57,29 @@ def _limit(storage: str, integer: bool) -> float:
     return INT_LIMIT[storage] if integer else math.inf
 
 
-def product_tile(x: np.ndarray, y: np.ndarray, kind: str, storage: str, integer: bool):
+def saturation_possible(x: np.ndarray, y: np.ndarray, storage: str, integer: bool) -> bool:
+    """The exact screen of _saturation_limit (matrix.py:297-312): no candidate
+    can overflow when max|x_fin| + max|y_fin| stays under the limit."""
+    bound = 0.0
+    for op in (x, y):
+        fin = op[np.isfinite(op)]
+        bound += float(np.max(np.abs(fin))) if fin.size else 0.0
+    limit = _limit(storage, integer)
+    if not math.isinf(limit):
+        return bound >= limit
+    return math.isinf(float(to_storage(np.array([bound]), storage)[0]))
+
+
+def product_tile(x: np.ndarray, y: np.ndarray, kind: str, storage: str, integer: bool, screen: bool = True):
     """One output block of the tropical product with the masked-overflow rule
     of _product_tile (matrix.py:315-346): candidates x[r,k] + y[k,c],
-    finite (x) finite sums that overflow / reach the integer limit -> ε."""
+    finite (x) finite sums that overflow / reach the integer limit -> ε.
+    ``screen=False`` skips the mask (the caller proved no overflow)."""
     with np.errstate(over="ignore", invalid="ignore"):
         block = x[:, :, None] + y[None, :, :]
     block = to_storage(block, storage)
+    if not screen:
+        return combine(kind).reduce(block, axis=1), False
     limit = _limit(storage, integer)
     bad = np.isinf(block) if math.isinf(limit) else (np.abs(block) >= limit)
     saturated = False
@@ -77,18 +93,30 @@ def product_tile(x: np.ndarray, y: np.ndarray, kind: str, storage: str, integer:
 
 
 def matmul(x: np.ndarray, y: np.ndarray, kind: str, storage: str = "f64", integer: bool = False,
-           acc: "np.ndarray | None" = None, tile_rows: int = 16, tile_cols: int = 256):
+           acc: "np.ndarray | None" = None, tile_rows: int = 16, tile_cols: int = 256, workers: int = 1):
     """Tropical product over output tiles, k never split (matrix.py:349-400).
+    ``workers`` > 1 fans the tiles over a thread pool exactly like the
+    reference (matrix.py:284-294,393-397; NumPy releases the GIL).
     Returns (oriented float64 result, saturated)."""
     assert x.shape[1] == y.shape[0]
     m, n = x.shape[0], y.shape[1]
     out = np.empty((m, n), dtype=np.float64)
-    saturated = False
-    for r0 in range(0, m, tile_rows):
-        for c0 in range(0, n, tile_cols):
-            blk, sat = product_tile(x[r0 : r0 + tile_rows], y[:, c0 : c0 + tile_cols], kind, storage, integer)
-            out[r0 : r0 + tile_rows, c0 : c0 + tile_cols] = blk
-            saturated |= sat
+    spans = [(r0, c0) for r0 in range(0, m, tile_rows) for c0 in range(0, n, tile_cols)]
+    screen = saturation_possible(x, y, storage, integer)
+
+    def run(span):
+        r0, c0 = span
+        blk, sat = product_tile(x[r0 : r0 + tile_rows], y[:, c0 : c0 + tile_cols], kind, storage, integer, screen)
+        out[r0 : r0 + tile_rows, c0 : c0 + tile_cols] = blk
+        return sat
+
+    if workers > 1 and len(spans) > 1:
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(max_workers=workers) as pool:
+            saturated = any(pool.map(run, spans))
+    else:
+        saturated = any([run(s) for s in spans])
     if acc is not None:
         combine(kind)(out, acc, out=out)
     return out, saturated

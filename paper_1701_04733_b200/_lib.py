@@ -87,6 +87,8 @@ SIGNATURES = {
         _i32,
         [_i32, _i32, _i32, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _i64, _i64, _i64, _p, _i64, _p, _p, _sz, _p],
     ),
+    "btas_gemm_timing": (_i32, [_i32]),
+    "btas_gemm_timing_read": (_i32, [ctypes.POINTER(_dbl), ctypes.POINTER(_i32)]),
     "btas_matvec": (_i32, [_i32, _i32, _i32, _p, _i64, _i64, _i64, _p, _i64, _i64, _p, _i64, _p, _p]),
     "btas_fw_workspace_bytes": (_sz, [_i32, _i64]),
     "btas_fw": (_i32, [_i32, _i32, _p, _i64, _i64, _i32, _dbl, _dbl, _p, _p, _sz, _p]),
@@ -134,6 +136,17 @@ def call(name: str, *args) -> None:
 
 def key_to_float(key: int) -> float:
     return float(load().btas_key_to_double(ctypes.c_ulonglong(key)))
+
+
+def gemm_timing(enable: bool) -> None:
+    call("btas_gemm_timing", 1 if enable else 0)
+
+
+def gemm_timing_read() -> "tuple[float, int]":
+    """(summed GEMM-kernel ms, number of bracketed btas_gemm calls); synchronises."""
+    ms, n = _dbl(), _i32()
+    call("btas_gemm_timing_read", ctypes.byref(ms), ctypes.byref(n))
+    return ms.value, n.value
 
 
 def probe_ceiling(mix: int) -> "dict[str, float]":

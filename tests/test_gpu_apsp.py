@@ -1,0 +1,196 @@
+"""GPU parity of APSP (blocked Floyd-Warshall and repeated squaring) against
+the reference's golden outputs and the pinned oracle — bit-exact distances,
+exact multiplication counts and negative-cycle flags."""
+
+import hashlib
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1701_04733_b200 as bt
+from paper_1701_04733_b200.graphs import dense_rows, instance_seed, random_graph_matrix
+from oracle import native as on
+from oracle import tropical as ot
+
+from gpu_helpers import DTYPES, MAX, MIN, STORAGE, f64bytes, symbolic
+
+pytestmark = pytest.mark.gpu
+
+
+def digest(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float64).tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_golden_apsp_triple_equivalence(cuda, golden, dtype):
+    """700 digraphs of test_acceptance.py:155-175: FW == squaring == the
+    reference, byte for byte, with the reference's multiplication counts."""
+    g = golden("apsp_small.npz")
+    meta = g["meta"]
+    for case in range(len(meta)):
+        adj = bt.TropicalMatrix(MIN, symbolic(g[f"adj{case}"]), dtype=dtype)
+        fw = bt.floyd_warshall(adj)
+        sq = bt.apsp_by_squaring(adj)
+        assert fw.distances.dist.to_numpy().tobytes() == f64bytes(g[f"fw{case}"]), case
+        assert sq.distances.dist.to_numpy().tobytes() == f64bytes(g[f"sq{case}"]), case
+        assert sq.multiplications_performed == meta[case][1]
+        assert fw.negative_cycle == bool(meta[case][2]) and sq.negative_cycle == bool(meta[case][3])
+        assert fw.algorithm is bt.Algorithm.FLOYD_WARSHALL and fw.multiplications_performed == 0
+        assert sq.algorithm is bt.Algorithm.REPEATED_SQUARING
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_golden_negative_cycles(cuda, golden, dtype):
+    """200 graphs with weights in [-3, 10] (test_acceptance.py:178-193): the
+    flags match; distances match too wherever no negative cycle exists."""
+    g = golden("negcycle.npz")
+    meta = g["meta"]
+    flagged = 0
+    for case in range(len(meta)):
+        adj = bt.TropicalMatrix(MIN, symbolic(g[f"adj{case}"]), dtype=dtype)
+        fw = bt.floyd_warshall(adj)
+        sq = bt.apsp_by_squaring(adj)
+        assert fw.negative_cycle == bool(meta[case][1]) and sq.negative_cycle == bool(meta[case][2]), case
+        assert sq.multiplications_performed == meta[case][3]
+        flagged += fw.negative_cycle
+        if not fw.negative_cycle:
+            assert fw.distances.dist.to_numpy().tobytes() == f64bytes(g[f"fw{case}"])
+            assert sq.distances.dist.to_numpy().tobytes() == f64bytes(g[f"sq{case}"])
+    assert 0 < flagged < len(meta)
+
+
+def test_golden_mult_counts(cuda, golden):
+    """n = 2..128 (test_acceptance.py:196-210): counts and result digests."""
+    g = golden("mult_count.npz")
+    for idx, (n, mults) in enumerate(g["meta"]):
+        adj = random_graph_matrix(int(n), 0.5, (1, 100), int(g["seeds"][idx]))
+        sq = bt.apsp_by_squaring(adj)
+        assert sq.multiplications_performed == mults
+        budget = 0 if n == 2 else 2 * math.ceil(math.log2(n - 1))
+        assert mults <= budget
+        assert digest(sq.distances.dist.to_numpy()) == str(g["sq_digest"][idx])
+        assert digest(bt.floyd_warshall(adj).distances.dist.to_numpy()) == str(g["fw_digest"][idx])
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_config_c1_apsp512(cuda, golden, dtype):
+    """BASELINE config C1 (n = 512, p = 0.5, weights 1..100,
+    instance_seed(1, 512)) — the case the reference CPU path runs in full."""
+    g = golden("c1_apsp512.npz")
+    seed = instance_seed(1, 512)
+    assert seed == int(g["seed"][0])
+    adj = random_graph_matrix(512, 0.5, (1, 100), seed, dtype=dtype)
+    assert digest(adj.to_numpy()) == str(g["adj_digest"][0])
+    sq = bt.apsp_by_squaring(adj)
+    assert sq.distances.dist.to_numpy().tobytes() == f64bytes(g["sq"])
+    assert sq.multiplications_performed == g["meta"][0] and not sq.negative_cycle
+    fw = bt.floyd_warshall(adj)
+    assert digest(fw.distances.dist.to_numpy()) == str(g["fw_digest"][0]) and not fw.negative_cycle
+
+
+def test_kats(cuda, golden):
+    g = golden("kat.npz")
+    three = bt.TropicalMatrix(MIN, symbolic(g["three_adj"]))
+    fw = bt.floyd_warshall(three)
+    assert fw.distances.dist.to_numpy().tobytes() == f64bytes(g["three_fw"])
+    assert fw.distances.dist.to_lists() == [[0, 1, 3], [math.inf, 0, 2], [math.inf, math.inf, 0]]
+    assert bt.apsp_by_squaring(three).distances.dist == fw.distances.dist
+    edgeless = bt.TropicalMatrix.filled(MIN, 4, 4)
+    for rep in (bt.floyd_warshall(edgeless), bt.apsp_by_squaring(edgeless)):
+        assert rep.distances.dist == bt.identity_matrix(MIN, 4) and not rep.negative_cycle
+    two = bt.TropicalMatrix(MIN, [[0, -2], [1, 0]])
+    assert bt.floyd_warshall(two).negative_cycle and bt.apsp_by_squaring(two).negative_cycle
+    one = bt.TropicalMatrix(MIN, [[0]])
+    rep = bt.apsp_by_squaring(one)
+    assert rep.distances.dist.to_lists() == [[0]] and rep.multiplications_performed == 0 and not rep.negative_cycle
+    loop = bt.TropicalMatrix(MIN, [[-1]])
+    assert bt.floyd_warshall(loop).negative_cycle and bt.apsp_by_squaring(loop).negative_cycle
+    k9 = bt.TropicalMatrix(MIN, [[0 if i == j else 1 for j in range(9)] for i in range(9)])
+    rep = bt.apsp_by_squaring(k9)
+    assert rep.multiplications_performed <= 2 and rep.distances.dist == bt.floyd_warshall(k9).distances.dist
+
+
+@pytest.mark.parametrize("dtype", [torch.int32, torch.float32])
+@pytest.mark.parametrize("n", [1000, 2500])
+def test_fw_equals_squaring_midsize(cuda, dtype, n):
+    """Config C3's cross-check at mid size: GPU blocked FW == GPU squaring,
+    and sampled rows equal the (pinned) row-closure oracle."""
+    adj = random_graph_matrix(n, 0.5, (1, 100), 4242 + n, dtype=dtype)
+    fw = bt.floyd_warshall(adj)
+    sq = bt.apsp_by_squaring(adj)
+    assert fw.distances.dist == sq.distances.dist
+    sym = np.concatenate([b for _, b in dense_rows(n, 0.5, (1, 100), 4242 + n)])
+    rows = [0, n // 3, n - 1]
+    want = ot.closure_rows(sym, rows, STORAGE[dtype], True,
+                           gemm=lambda a, b: on.matmul(a, b, "minplus", STORAGE[dtype], True)[0])
+    got = fw.distances.dist.to_numpy()[rows]
+    assert got.tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_fw_negative_weights_and_sparse(cuda, dtype):
+    """Negative weights without negative cycles (no s16 shortcut for the
+    pivots that leave its domain) and sparse graphs with long paths, vs the
+    sequential C oracle FW."""
+    for n, p, wr, seed in ((700, 0.02, (0, 100), 1), (333, 0.5, (-1, 60), 2), (300, 0.01, (1, 5000), 3)):
+        sym = np.concatenate([b for _, b in dense_rows(n, p, wr, seed)])
+        adj = bt.TropicalMatrix(MIN, sym, dtype=dtype)
+        want, neg, _ = on.floyd_warshall_rounds(ot.closure_base(sym), STORAGE[dtype], True)
+        fw = bt.floyd_warshall(adj)
+        assert fw.negative_cycle == neg
+        if not neg:
+            assert fw.distances.dist.to_numpy().tobytes() == want.tobytes(), (n, p, wr)
+            assert bt.apsp_by_squaring(adj).distances.dist == fw.distances.dist
+
+
+def test_fw_masked_path(cuda):
+    """When the reference screen 2(n+1)max|x| < limit fails (apsp.py:103-107)
+    the masked rounds run; results and flag match the oracle."""
+    rng = np.random.default_rng(8)
+    n = 80
+    sym = rng.integers(1, 10**7, (n, n)).astype(float)
+    sym[rng.random((n, n)) < 0.6] = math.inf
+    np.fill_diagonal(sym, 0)
+    for dtype in (torch.int32, torch.float64):
+        adj = bt.TropicalMatrix(MIN, sym, dtype=dtype)
+        bt.reset_saturation()
+        fw = bt.floyd_warshall(adj)
+        want, neg, sat = ot.floyd_warshall(ot.orient("minplus", sym), STORAGE[dtype], True)
+        assert fw.distances.dist.to_numpy().tobytes() == want.tobytes()
+        assert bt.saturation_seen() == sat
+
+
+def test_verifier(cuda):
+    adj = random_graph_matrix(40, 0.3, (0, 100), 5)
+    rep = bt.floyd_warshall(adj)
+    assert bt.verify_apsp(adj, rep.distances)
+    assert bt.verify_apsp(adj, bt.apsp_by_squaring(adj).distances)
+    three = bt.TropicalMatrix(MIN, [[0, 1, 5], [math.inf, 0, 2], [math.inf, math.inf, 0]])
+    stale = bt.TropicalMatrix(MIN, [[0, 1, 5], [math.inf, 0, 2], [math.inf, math.inf, 0]])
+    v = bt.find_apsp_violation(three, bt.DistanceMatrix.from_matrix(stale))
+    assert v is not None and ("triangle" in v or "fixpoint" in v)
+    good = bt.floyd_warshall(three).distances.dist.to_lists()
+    broken = [r[:] for r in good]
+    broken[1][1] = 2.0
+    assert "diagonal" in bt.find_apsp_violation(three, bt.DistanceMatrix.from_matrix(bt.TropicalMatrix(MIN, broken)))
+    above = [r[:] for r in good]
+    above[0][1] = 9.0
+    assert "edge" in bt.find_apsp_violation(three, bt.DistanceMatrix.from_matrix(bt.TropicalMatrix(MIN, above)))
+
+
+def test_input_errors(cuda):
+    rect = bt.TropicalMatrix(MIN, [[0, 1, 2], [3, 0, 4]])
+    wrong = bt.TropicalMatrix(MAX, [[0]])
+    for solver in (bt.floyd_warshall, bt.apsp_by_squaring):
+        with pytest.raises(bt.DimensionMismatch):
+            solver(rect)
+        with pytest.raises(bt.SemiringMismatch):
+            solver(wrong)
+        with pytest.raises(TypeError):
+            solver([[0]])
+    with pytest.raises(ValueError):
+        bt.DistanceMatrix(2, bt.TropicalMatrix(MAX, [[0, 1], [1, 0]]))
+    with pytest.raises(bt.DimensionMismatch):
+        bt.DistanceMatrix(3, bt.identity_matrix(MIN, 2))
