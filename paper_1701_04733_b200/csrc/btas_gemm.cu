@@ -75,13 +75,24 @@ struct GemmGeometry {
 
 inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// column groups of the s16x2 microtile (4: 128-wide tiles, 8: 256-wide);
+// BTAS_S16_GN overrides for A/B measurements
+int s16_gn() {
+  static int gn = [] {
+    const char* e = getenv("BTAS_S16_GN");
+    const int v = e ? atoi(e) : 8;
+    return v == 4 ? 4 : 8;
+  }();
+  return gn;
+}
+
 WsLayout ws_layout(int dtype, int64_t M, int64_t N, int64_t K) {
   const size_t es = dtype == BTAS_F64 ? 8 : 4;
   const int64_t BM = dtype == BTAS_F64 ? 64 : 128, BN = 128;
   const int64_t Kp = round_up(K, 2 * kKP);               // 32-bit/64-bit paths
   const int64_t Kw = round_up(ceil_div(K, 2), 2 * kKP);  // s16 words
   const int64_t Mp = round_up(M, BM), Np = round_up(N, BN);
-  const int64_t Mp16 = round_up(M, 128), Np16 = round_up(N, 128);
+  const int64_t Mp16 = round_up(M, 128), Np16 = round_up(N, 256);
   const size_t a32 = (size_t)Mp * Kp * es, b32 = (size_t)Np * Kp * es;
   const size_t a16 = (size_t)Mp16 * Kw * 4, b16 = (size_t)Np16 * Kw * 4;
   WsLayout L;
@@ -384,10 +395,11 @@ int gemm_typed(int integer_mode, const T* A, int64_t lda, const T* B, int64_t ld
     g.skip_lo = g.skip_hi = 0;
   }
   GemmArgs g16{};  // int16x2 path (integer operands with |x| < 2^12)
+  const int bn16 = 32 * s16_gn();
   if (int_mode) {
     const int64_t Kv = ceil_div(K, 2);              // words
     const int64_t Kp2 = round_up(Kv, 2 * kKP) / 2;  // word pairs
-    const int64_t Mp = round_up(M, 128), Np = round_up(N, 128);
+    const int64_t Mp = round_up(M, 128), Np = round_up(N, bn16);
     uint32_t* Ap = reinterpret_cast<uint32_t*>(ws + L.packA);
     uint32_t* Bp = reinterpret_cast<uint32_t*>(ws + L.packB);
     dim3 ga((unsigned)ceil_div(2 * Kp2, 64), (unsigned)ceil_div(Mp, 32));
@@ -395,16 +407,20 @@ int gemm_typed(int integer_mode, const T* A, int64_t lda, const T* B, int64_t ld
                                                                     BTAS_PATH_S16X2, BTAS_PATH_S16X2);
     // B: virtual rows are words along k: rows of the virtual matrix = Kv
     const int64_t tb = Kp2 * Np;
-    pack_b_kernel<T, uint32_t, true, MIN, 128>
-        <<<(unsigned)std::min<int64_t>(ceil_div(tb, 256), 65535), 256, 0, st>>>(B, ldb, K, N, Np, Kp2, Bp, ctrl,
-                                                                         BTAS_PATH_S16X2, BTAS_PATH_S16X2);
+    const unsigned gb = (unsigned)std::min<int64_t>(ceil_div(tb, 256), 65535);
+    if (bn16 == 256)
+      pack_b_kernel<T, uint32_t, true, MIN, 256><<<gb, 256, 0, st>>>(B, ldb, K, N, Np, Kp2, Bp, ctrl,
+                                                                      BTAS_PATH_S16X2, BTAS_PATH_S16X2);
+    else
+      pack_b_kernel<T, uint32_t, true, MIN, 128><<<gb, 256, 0, st>>>(B, ldb, K, N, Np, Kp2, Bp, ctrl,
+                                                                      BTAS_PATH_S16X2, BTAS_PATH_S16X2);
     BTAS_CUDA_CHECK_LAUNCH();
     g16 = g;
     g16.Ap = Ap;
     g16.Bp = Bp;
     g16.Kp2 = Kp2;
     g16.mblocks = (int)(Mp / 128);
-    g16.nblocks = (int)(Np / 128);
+    g16.nblocks = (int)(Np / bn16);
     g16.gate_value = BTAS_PATH_S16X2;
     g16.integer_mode = 1;
     g16.limit = limit;
@@ -422,7 +438,8 @@ int gemm_typed(int integer_mode, const T* A, int64_t lda, const T* B, int64_t ld
   rc = launch_tropical_gemm<MixChecked<T, MIN>, MIN>(g, st);
   if (rc) return rc;
   if (int_mode) {
-    rc = launch_tropical_gemm<MixS16<MIN, T>, MIN>(g16, st);
+    rc = bn16 == 256 ? launch_tropical_gemm<MixS16<MIN, T, 8>, MIN>(g16, st)
+                     : launch_tropical_gemm<MixS16<MIN, T, 4>, MIN>(g16, st);
     if (rc) return rc;
   }
   timing_end(st, t0);

@@ -129,12 +129,14 @@ struct MixF64 {
 
 // int16x2 lanes: E is a word holding (k even, k odd) entries; acc lanes hold
 // the running ⊕ of even-k and odd-k candidates, merged in finish().
-template <bool MIN, class OutT>
+template <bool MIN, class OutT, int GNv = 4>
 struct MixS16 {
   using E = uint32_t;
   using Acc = uint32_t;
   using Out = OutT;
-  static constexpr int GM = 4, GN = 4, KP = 16, STAGES = 4;
+  // GNv = 8: 128 x 256 tiles, 8 x 16 microtile (12 LDS.128 per 256 DPX ops
+  // instead of 8 per 128)
+  static constexpr int GM = 4, GN = GNv, KP = 16, STAGES = 4;
   static constexpr int path = BTAS_PATH_S16X2;
   static constexpr bool kChecked = false;
   BTAS_D static Acc init() {
