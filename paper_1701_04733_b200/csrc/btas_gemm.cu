@@ -75,13 +75,13 @@ struct GemmGeometry {
 
 inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-// column groups of the s16x2 microtile (4: 128-wide tiles, 8: 256-wide);
-// BTAS_S16_GN overrides for A/B measurements
+// column groups of the s16x2 microtile: 4 = 128-wide tiles (default), 8 =
+// 256-wide, 8x16 microtile (fewer LDS per DPX op but measured 1 % slower,
+// profiles/r01_experiments.md); BTAS_S16_GN=8 selects it for A/B runs
 int s16_gn() {
   static int gn = [] {
     const char* e = getenv("BTAS_S16_GN");
-    const int v = e ? atoi(e) : 8;
-    return v == 4 ? 4 : 8;
+    return (e && atoi(e) == 8) ? 8 : 4;
   }();
   return gn;
 }

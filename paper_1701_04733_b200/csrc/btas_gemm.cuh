@@ -31,7 +31,9 @@
 namespace btas {
 
 constexpr int kConsumerWarps = 8;
-constexpr int kGemmThreads = (kConsumerWarps + 1) * 32;
+constexpr int kGemmThreads = (kConsumerWarps + 4) * 32;  // producer warpgroup + 2 consumer warpgroups
+constexpr int kProducerRegs = 40;
+constexpr int kConsumerRegs = 232;  // 4*40*32 + 8*232*32 = 64512 <= 65536
 
 // ---------------------------------------------------------------------------
 // epilogue / kernel arguments
@@ -301,18 +303,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
     return (r0 >= g.skip_lo && r0 + BM <= g.skip_hi) || (c0 >= g.skip_lo && c0 + BN <= g.skip_hi);
   };
 
-  if (warp == kConsumerWarps) {
-    // ------------------------------ producer ------------------------------
-    if (lane == 0) {
-      const E* Ap = static_cast<const E*>(g.Ap);
-      const E* Bp = static_cast<const E*>(g.Bp);
+  // ------------------------------ producer --------------------------------
+  // Warp-specialised: warpgroup 0 gives its registers back (setmaxnreg) and
+  // one elected thread streams the k-stages with bulk TMA copies into the
+  // STAGES-deep mbarrier ring; warpgroups 1-2 (8 warps) compute with up to
+  // kConsumerRegs registers per thread.
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
+    if (warp == 0 && lane == 0) {
       uint32_t it = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         int mb, nb;
         tile_coords(tile, g.mblocks, g.nblocks, mb, nb);
         if (skipped(mb, nb)) continue;
-        const E* gA = Ap + (size_t)mb * g.Kp2 * BM * 2;
-        const E* gB = Bp + (size_t)nb * g.Kp2 * BN * 2;
+        const E* gA = static_cast<const E*>(g.Ap) + (size_t)mb * g.Kp2 * BM * 2;
+        const E* gB = static_cast<const E*>(g.Bp) + (size_t)nb * g.Kp2 * BN * 2;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % ST;
           if (it >= (uint32_t)ST) mbar_wait(&empty[s], ((it / ST) - 1) & 1);
@@ -324,10 +329,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
     }
     return;
   }
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kConsumerRegs));
 
   // ------------------------------ consumers -------------------------------
-  const int ty = (warp >> 1) * 4 + (lane >> 3);  // 0..15
-  const int tx = (warp & 1) * 8 + (lane & 7);    // 0..15
+  const int cw = warp - 4;                     // consumer warp 0..7
+  const int ty = (cw >> 1) * 4 + (lane >> 3);  // 0..15
+  const int tx = (cw & 1) * 8 + (lane & 7);    // 0..15
   bool changed = false, diag_neg = false, sat = false;
   uint32_t it = 0;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
