@@ -32,30 +32,42 @@ struct FwCtrl {
   int32_t pad[63];
 };
 
-// relaxation candidate of one round
-template <class T, bool CHECKED>
-BTAS_D T fw_cand(T a, T b, int int_mode, double limit, bool& sat) {
-  T s = a + b;
-  if constexpr (CHECKED) {
-    bool over;
-    if constexpr (Traits<T>::dtype == BTAS_I32) over = (s >= (T)kI32Limit) || (s <= -(T)kI32Limit);
-    else over = int_mode ? (fabs((double)s) >= limit) : isinf((double)s);
-    if (over && Traits<T>::finite(a) && Traits<T>::finite(b)) {
-      sat = true;
-      return Traits<T>::eps(true);
-    }
-  }
-  if constexpr (Traits<T>::dtype == BTAS_I32) {
-    // canonical Inf; clamp inside negative cycles so int32 never wraps
-    if (s >= (T)kI32Limit) return (T)kI32Inf;
-    if (s < -(T)kI32Limit) return (T)(-kI32Limit);
-  }
-  return s;
-}
+// ------------------------------------------------------------------ rounds
+// Relaxation modes of one round's candidate d = min(d, a (x) b):
+//   kFast     a + b straight into the add-min (VIADDMNMX / FADD+FMNMX):
+//             int32 with no negative weight (values stay in [0, Inf]) and
+//             every float storage (IEEE Inf absorbs)
+//   kClamp    int32 with negative weights: canonical Inf, and a clamp at
+//             -2^28 so a negative cycle can never wrap int32
+//   kChecked  the reference's masked rounds (apsp.py:111-123)
+enum { kFast = 0, kClamp = 1, kChecked = 2 };
 
-template <class T>
-BTAS_D T tmin(T a, T b) {
-  return b < a ? b : a;
+template <class T, int MODE>
+BTAS_D void relax(T& d, T a, T b, int int_mode, double limit, bool& sat) {
+  if constexpr (MODE == kFast) {
+    if constexpr (Traits<T>::dtype == BTAS_I32) {
+      d = __viaddmin_s32(a, b, d);
+    } else {
+      const T s = a + b;
+      d = s < d ? s : d;
+    }
+  } else {
+    T s = a + b;
+    if constexpr (MODE == kChecked) {
+      bool over;
+      if constexpr (Traits<T>::dtype == BTAS_I32) over = (s >= (T)kI32Limit) || (s <= -(T)kI32Limit);
+      else over = int_mode ? (fabs((double)s) >= limit) : isinf((double)s);
+      if (over && Traits<T>::finite(a) && Traits<T>::finite(b)) {
+        sat = true;
+        s = Traits<T>::eps(true);
+      }
+    }
+    if constexpr (Traits<T>::dtype == BTAS_I32) {
+      if (s >= (T)kI32Limit) s = (T)kI32Inf;
+      if (s < -(T)kI32Limit) s = (T)(-kI32Limit);
+    }
+    d = s < d ? s : d;
+  }
 }
 
 template <class T>
@@ -73,11 +85,12 @@ BTAS_D uint32_t s16_lane(T v) {
 template <class T>
 struct FwB {
   static constexpr int b = sizeof(T) == 8 ? 64 : 128;  // pivot block (phase-3 K)
+  static constexpr int R = b / 16;                      // per-thread sub-block edge (16 x 16 threads)
 };
+constexpr int kFwThreads = 256;
 
 struct FwArgs {
   int64_t n, ld, k0;
-  int b;
   int nblk;
   int int_mode;
   double limit;
@@ -89,125 +102,189 @@ struct FwArgs {
   FwCtrl* ctrl;
 };
 
-// ------------------------------------------------------------------ phase 1
-// smem: tile[b][b+1], rs[b][b] (row snapshots), cs[b][b] (col snapshots as [a][k'])
-template <class T, bool CHECKED>
-__global__ void __launch_bounds__(512) fw_phase1_kernel(T* __restrict__ D, T* __restrict__ rowsnapP,
-                                                        T* __restrict__ colsnapP, T* __restrict__ Scol,
-                                                        T* __restrict__ Srow, uint32_t* __restrict__ Scol16,
-                                                        uint32_t* __restrict__ Srow16, FwArgs f) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int b = FwB<T>::b, bp = b + 1;
-  T* tile = reinterpret_cast<T*>(smem_raw);
-  T* rs = tile + b * bp;
-  T* cs = rs + b * b;
+// The tile lives in registers: thread (ty, tx) of a 16 x 16 grid owns rows
+// ty*R .. +R and cols tx*R .. +R.  Round k: the owners of row k / column k
+// publish the PRE-round values into the history arrays (which double as the
+// round's operand buffers — written once, so one barrier per round), then
+// every thread relaxes its R x R block.
+template <class T>
+BTAS_D void load_block(const T* __restrict__ D, const FwArgs& f, int64_t r0, int64_t c0, int ty, int tx,
+                       T (&v)[FwB<T>::R][FwB<T>::R]) {
+  constexpr int R = FwB<T>::R;
   const T inf = Traits<T>::eps(true);
-  if (threadIdx.x == 0) f.ctrl->s16_overflow = 0;
-  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
-    const int a = e / b, c = e - a * b;
-    const int64_t i = f.k0 + a, j = f.k0 + c;
-    tile[a * bp + c] = (i < f.n && j < f.n) ? D[i * f.ld + j] : inf;
-  }
-  bool sat = false;
-  for (int k = 0; k < b; ++k) {
-    __syncthreads();
-    for (int c = threadIdx.x; c < b; c += blockDim.x) {
-      rs[k * b + c] = tile[k * bp + c];
-      cs[c * b + k] = tile[c * bp + k];
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
-      const int a = e / b, c = e - a * b;
-      const T s = fw_cand<T, CHECKED>(cs[a * b + k], rs[k * b + c], f.int_mode, f.limit, sat);
-      tile[a * bp + c] = tmin(tile[a * bp + c], s);
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int64_t row = r0 + ty * R + i;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int64_t col = c0 + tx * R + j;
+      v[i][j] = (row < f.n && col < f.n) ? D[row * f.ld + col] : inf;
     }
   }
-  __syncthreads();
+}
+
+template <class T>
+BTAS_D void store_block(T* __restrict__ D, const FwArgs& f, int64_t r0, int64_t c0, int ty, int tx,
+                        const T (&v)[FwB<T>::R][FwB<T>::R]) {
+  constexpr int R = FwB<T>::R;
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int64_t row = r0 + ty * R + i;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int64_t col = c0 + tx * R + j;
+      if (row < f.n && col < f.n) D[row * f.ld + col] = v[i][j];
+    }
+  }
+}
+
+// packed phase-3 operands from a history array h[k][x] (k = pivot round,
+// x = row (A operand, Scol) or col (B operand, Srow) inside the block at rc0)
+template <class T>
+BTAS_D bool emit_history(const T* __restrict__ h, int64_t rc0, int BLK, const FwArgs& f, T* __restrict__ P,
+                         uint32_t* __restrict__ P16) {
+  constexpr int b = FwB<T>::b;
   bool out16 = false;
-  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
-    const int a = e / b, c = e - a * b;
-    const int64_t i = f.k0 + a, j = f.k0 + c;
-    if (i < f.n && j < f.n) D[i * f.ld + j] = tile[a * bp + c];
-    rowsnapP[e] = rs[e];
-    colsnapP[e] = cs[e];
-    // pivot rows of Scol (A operand: row i, k = c) and pivot cols of Srow (B: k = a, col j)
-    Scol[packed_index(i, c, f.Kp2, f.BMa)] = cs[a * b + c];
-    Srow[packed_index(f.k0 + c, a, f.Kp2, f.BNb)] = rs[a * b + c];
-    out16 |= !s16_ok(cs[e]) || !s16_ok(rs[e]);
+  for (int e = threadIdx.x; e < (b / 2) * b; e += blockDim.x) {
+    const int kp = e / b, x = e - kp * b;
+    const T v0 = h[(2 * kp) * b + x], v1 = h[(2 * kp + 1) * b + x];
+    const int64_t idx = packed_index(rc0 + x, 2 * kp, f.Kp2, BLK);
+    P[idx] = v0;
+    P[idx + 1] = v1;
+    out16 |= !s16_ok(v0) || !s16_ok(v1);
   }
   if (f.emit_s16) {
-    // words: lanes (k even, k odd)
-    for (int e = threadIdx.x; e < b * (b / 2); e += blockDim.x) {
-      const int a = e / (b / 2), w = e - a * (b / 2);
-      const int64_t i = f.k0 + a;
-      Scol16[packed_index(i, w, f.Kp2w, 128)] = s16_lane(cs[a * b + 2 * w]) | (s16_lane(cs[a * b + 2 * w + 1]) << 16);
-      const int64_t j = f.k0 + a;  // here a indexes the column
-      Srow16[packed_index(j, w, f.Kp2w, 128)] =
-          s16_lane(rs[(2 * w) * b + a]) | (s16_lane(rs[(2 * w + 1) * b + a]) << 16);
+    for (int e = threadIdx.x; e < (b / 4) * b; e += blockDim.x) {
+      const int wp = e / b, x = e - wp * b;
+      const int k = 4 * wp;
+      const uint32_t w0 = s16_lane(h[k * b + x]) | (s16_lane(h[(k + 1) * b + x]) << 16);
+      const uint32_t w1 = s16_lane(h[(k + 2) * b + x]) | (s16_lane(h[(k + 3) * b + x]) << 16);
+      const int64_t idx = packed_index(rc0 + x, 2 * wp, f.Kp2w, 128);
+      P16[idx] = w0;
+      P16[idx + 1] = w1;
     }
   }
+  return out16;
+}
+
+// ------------------------------------------------------------------ phase 1
+// smem: rs[k][c] (pivot-row history), cT[k][a] (pivot-column history)
+template <class T, int MODE>
+__global__ void __launch_bounds__(kFwThreads) fw_phase1_kernel(T* __restrict__ D, T* __restrict__ rowsnapP,
+                                                               T* __restrict__ colsnapT, T* __restrict__ Scol,
+                                                               T* __restrict__ Srow, uint32_t* __restrict__ Scol16,
+                                                               uint32_t* __restrict__ Srow16, FwArgs f) {
+  constexpr int b = FwB<T>::b, R = FwB<T>::R;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* rs = reinterpret_cast<T*>(smem_raw);
+  T* cT = rs + b * b;
+  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+  if (threadIdx.x == 0) f.ctrl->s16_overflow = 0;
+  T v[R][R];
+  load_block(D, f, f.k0, f.k0, ty, tx, v);
+  bool sat = false;
+  for (int kb = 0; kb < b; kb += R) {
+    const int owner = kb / R;
+#pragma unroll
+    for (int kk = 0; kk < R; ++kk) {
+      const int k = kb + kk;
+      if (ty == owner) {
+#pragma unroll
+        for (int j = 0; j < R; ++j) rs[k * b + tx * R + j] = v[kk][j];
+      }
+      if (tx == owner) {
+#pragma unroll
+        for (int i = 0; i < R; ++i) cT[k * b + ty * R + i] = v[i][kk];
+      }
+      __syncthreads();
+      T rowv[R], colv[R];
+#pragma unroll
+      for (int j = 0; j < R; ++j) rowv[j] = rs[k * b + tx * R + j];
+#pragma unroll
+      for (int i = 0; i < R; ++i) colv[i] = cT[k * b + ty * R + i];
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+#pragma unroll
+        for (int j = 0; j < R; ++j) relax<T, MODE>(v[i][j], colv[i], rowv[j], f.int_mode, f.limit, sat);
+    }
+  }
+  store_block(D, f, f.k0, f.k0, ty, tx, v);
+  __syncthreads();
+  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
+    rowsnapP[e] = rs[e];
+    colsnapT[e] = cT[e];
+  }
+  // pivot rows of Scol (A operand) and pivot columns of Srow (B operand)
+  bool out16 = emit_history(cT, f.k0, f.BMa, f, Scol, Scol16);
+  out16 |= emit_history(rs, f.k0, f.BNb, f, Srow, Srow16);
   if (__syncthreads_or(out16) && threadIdx.x == 0) atomicOr(&f.ctrl->s16_overflow, 1);
-  if (CHECKED && __any_sync(0xffffffffu, sat) && (threadIdx.x & 31) == 0) atomicOr(&f.flags[BTAS_FLAG_SATURATED], 1);
+  if (MODE == kChecked && __any_sync(0xffffffffu, sat) && (threadIdx.x & 31) == 0)
+    atomicOr(&f.flags[BTAS_FLAG_SATURATED], 1);
 }
 
 // ------------------------------------------------------------------ phase 2
-// blockIdx.y == 0: row panel (pivot rows, column block blockIdx.x)
-// blockIdx.y == 1: column panel (row block blockIdx.x, pivot columns)
-template <class T, bool CHECKED>
-__global__ void __launch_bounds__(512) fw_phase2_kernel(T* __restrict__ D, const T* __restrict__ rowsnapP,
-                                                        const T* __restrict__ colsnapP, T* __restrict__ Scol,
-                                                        T* __restrict__ Srow, uint32_t* __restrict__ Scol16,
-                                                        uint32_t* __restrict__ Srow16, FwArgs f) {
+// blockIdx.y == 0: row panel (pivot rows x column block blockIdx.x), its own
+//                  row k each round, pivot-column snapshots fixed in smem
+// blockIdx.y == 1: column panel (row block blockIdx.x x pivot columns)
+template <class T, int MODE>
+__global__ void __launch_bounds__(kFwThreads) fw_phase2_kernel(T* __restrict__ D, const T* __restrict__ rowsnapP,
+                                                               const T* __restrict__ colsnapT, T* __restrict__ Scol,
+                                                               T* __restrict__ Srow, uint32_t* __restrict__ Scol16,
+                                                               uint32_t* __restrict__ Srow16, FwArgs f) {
+  constexpr int b = FwB<T>::b, R = FwB<T>::R;
   const int blk = blockIdx.x;
-  if (blk == (int)(f.k0 / f.b)) return;
+  if (blk == (int)(f.k0 / b)) return;
   const bool row_panel = blockIdx.y == 0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int b = FwB<T>::b, bp = b + 1;
-  T* tile = reinterpret_cast<T*>(smem_raw);
-  T* ps = tile + b * bp;  // pivot snapshots (b x b)
-  T* buf = ps + b * b;    // [2][b] this round's snapshot (double-buffered)
-  const T inf = Traits<T>::eps(true);
+  T* fixed = reinterpret_cast<T*>(smem_raw);  // row panel: colsnapT[k][a]; col panel: rowsnapP[k][c]
+  T* hist = fixed + b * b;                      // row panel: rs[k][c];      col panel: cT[k][a]
+  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
   const int64_t r0 = row_panel ? f.k0 : (int64_t)blk * b;
   const int64_t c0 = row_panel ? (int64_t)blk * b : f.k0;
-  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
-    const int a = e / b, c = e - a * b;
-    const int64_t i = r0 + a, j = c0 + c;
-    tile[a * bp + c] = (i < f.n && j < f.n) ? D[i * f.ld + j] : inf;
-    ps[e] = row_panel ? colsnapP[e] : rowsnapP[e];  // colsnapP[a][k'] / rowsnapP[k'][c]
+  {
+    const T* src = row_panel ? colsnapT : rowsnapP;
+    for (int e = threadIdx.x; e < b * b; e += blockDim.x) fixed[e] = src[e];
   }
-  bool sat = false, out16 = false;
-  for (int k = 0; k < b; ++k) {
-    T* cur = buf + (k & 1) * b;
-    __syncthreads();
-    for (int x = threadIdx.x; x < b; x += blockDim.x) cur[x] = row_panel ? tile[k * bp + x] : tile[x * bp + k];
-    __syncthreads();
-    for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
-      const int a = e / b, c = e - a * b;
-      const T s = row_panel ? fw_cand<T, CHECKED>(ps[a * b + k], cur[c], f.int_mode, f.limit, sat)
-                            : fw_cand<T, CHECKED>(cur[a], ps[k * b + c], f.int_mode, f.limit, sat);
-      tile[a * bp + c] = tmin(tile[a * bp + c], s);
-    }
-    // emit this round's snapshot (k = pivot index) into the phase-3 operands
-    for (int x = threadIdx.x; x < b; x += blockDim.x) {
-      const T v = cur[x];
-      out16 |= !s16_ok(v);
-      if (row_panel) Srow[packed_index(c0 + x, k, f.Kp2, f.BNb)] = v;
-      else Scol[packed_index(r0 + x, k, f.Kp2, f.BMa)] = v;
-      if (f.emit_s16 && (k & 1)) {
-        const uint32_t w = s16_lane(buf[x]) | (s16_lane(v) << 16);
-        if (row_panel) Srow16[packed_index(c0 + x, k >> 1, f.Kp2w, 128)] = w;
-        else Scol16[packed_index(r0 + x, k >> 1, f.Kp2w, 128)] = w;
+  T v[R][R];
+  load_block(D, f, r0, c0, ty, tx, v);
+  bool sat = false;
+  for (int kb = 0; kb < b; kb += R) {
+    const int owner = kb / R;
+#pragma unroll
+    for (int kk = 0; kk < R; ++kk) {
+      const int k = kb + kk;
+      if (row_panel) {
+        if (ty == owner) {
+#pragma unroll
+          for (int j = 0; j < R; ++j) hist[k * b + tx * R + j] = v[kk][j];
+        }
+      } else {
+        if (tx == owner) {
+#pragma unroll
+          for (int i = 0; i < R; ++i) hist[k * b + ty * R + i] = v[i][kk];
+        }
       }
+      __syncthreads();
+      T rowv[R], colv[R];
+      const T* rsrc = row_panel ? hist : fixed;  // [k][c]
+      const T* csrc = row_panel ? fixed : hist;  // [k][a]
+#pragma unroll
+      for (int j = 0; j < R; ++j) rowv[j] = rsrc[k * b + tx * R + j];
+#pragma unroll
+      for (int i = 0; i < R; ++i) colv[i] = csrc[k * b + ty * R + i];
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+#pragma unroll
+        for (int j = 0; j < R; ++j) relax<T, MODE>(v[i][j], colv[i], rowv[j], f.int_mode, f.limit, sat);
     }
   }
+  store_block(D, f, r0, c0, ty, tx, v);
   __syncthreads();
-  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
-    const int a = e / b, c = e - a * b;
-    const int64_t i = r0 + a, j = c0 + c;
-    if (i < f.n && j < f.n) D[i * f.ld + j] = tile[a * bp + c];
-  }
+  const bool out16 = row_panel ? emit_history(hist, c0, f.BNb, f, Srow, Srow16)
+                               : emit_history(hist, r0, f.BMa, f, Scol, Scol16);
   if (__syncthreads_or(out16) && threadIdx.x == 0) atomicOr(&f.ctrl->s16_overflow, 1);
-  if (CHECKED && __any_sync(0xffffffffu, sat) && (threadIdx.x & 31) == 0) atomicOr(&f.flags[BTAS_FLAG_SATURATED], 1);
+  if (MODE == kChecked && __any_sync(0xffffffffu, sat) && (threadIdx.x & 31) == 0)
+    atomicOr(&f.flags[BTAS_FLAG_SATURATED], 1);
 }
 
 __global__ void fill_u32_kernel(uint32_t* p, int64_t n, uint32_t v) {
@@ -274,7 +351,7 @@ FwWs fw_ws(int64_t n) {
   return w;
 }
 
-template <class T, bool CHECKED>
+template <class T, int MODE>
 int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, double min_finite, int32_t* flags,
              unsigned char* ws, cudaStream_t st) {
   using G = FwGeom<T>;
@@ -284,7 +361,7 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
   const bool int_mode = Traits<T>::dtype == BTAS_I32 || integer_mode;
   const double limit = Traits<T>::dtype == BTAS_I32 ? (double)kI32Limit : Traits<T>::int_limit;
   (void)max_abs;
-  (void)min_finite;
+  constexpr bool CHECKED = MODE == kChecked;
 
   FwCtrl* ctrl = reinterpret_cast<FwCtrl*>(ws + W.ctrl);
   T* rsp = reinterpret_cast<T*>(ws + W.rsp);
@@ -306,7 +383,6 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
   FwArgs f{};
   f.n = n;
   f.ld = ld;
-  f.b = b;
   f.nblk = nblk;
   f.int_mode = int_mode ? 1 : 0;
   f.limit = limit;
@@ -318,13 +394,13 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
   f.flags = flags;
   f.ctrl = ctrl;
 
-  const size_t smem1 = ((size_t)b * (b + 1) + 2 * (size_t)b * b) * sizeof(T);
-  const size_t smem2 = ((size_t)b * (b + 1) + (size_t)b * b + 2 * (size_t)b) * sizeof(T);
+  const size_t smem1 = 2 * (size_t)b * b * sizeof(T);
+  const size_t smem2 = 2 * (size_t)b * b * sizeof(T);
   static bool configured = false;
   if (!configured) {
-    if (cudaFuncSetAttribute(fw_phase1_kernel<T, CHECKED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(fw_phase1_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem1) != cudaSuccess ||
-        cudaFuncSetAttribute(fw_phase2_kernel<T, CHECKED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(fw_phase2_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem2) != cudaSuccess) {
       (void)cudaGetLastError();
       return BTAS_ERR_CUDA;
@@ -364,9 +440,9 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
 
   for (int kb = 0; kb < nblk; ++kb) {
     f.k0 = (int64_t)kb * b;
-    fw_phase1_kernel<T, CHECKED><<<1, 512, smem1, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
+    fw_phase1_kernel<T, MODE><<<1, kFwThreads, smem1, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
     if (nblk > 1) {
-      fw_phase2_kernel<T, CHECKED><<<dim3(nblk, 2), 512, smem2, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
+      fw_phase2_kernel<T, MODE><<<dim3(nblk, 2), kFwThreads, smem2, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
     }
     BTAS_CUDA_CHECK_LAUNCH();
     if (nblk > 1) {
@@ -420,9 +496,12 @@ extern "C" int btas_fw(int dtype, int integer_mode, void* D, int64_t ld, int64_t
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   unsigned char* ws = static_cast<unsigned char*>(workspace);
   int rc;
-#define BTAS_FW_CALL(T)                                                                                  \
-  (masked ? fw_typed<T, true>(integer_mode, (T*)D, ld, n, max_abs, min_finite, dev_flags, ws, st)        \
-          : fw_typed<T, false>(integer_mode, (T*)D, ld, n, max_abs, min_finite, dev_flags, ws, st))
+  // int32 with a negative weight needs the clamped rounds; floats never do
+#define BTAS_FW_CALL(T)                                                                                      \
+  (masked ? fw_typed<T, kChecked>(integer_mode, (T*)D, ld, n, max_abs, min_finite, dev_flags, ws, st)        \
+   : (dtype == BTAS_I32 && min_finite < 0.0)                                                                 \
+       ? fw_typed<T, kClamp>(integer_mode, (T*)D, ld, n, max_abs, min_finite, dev_flags, ws, st)             \
+       : fw_typed<T, kFast>(integer_mode, (T*)D, ld, n, max_abs, min_finite, dev_flags, ws, st))
   switch (dtype) {
     case BTAS_F32:
       rc = BTAS_FW_CALL(float);

@@ -237,6 +237,35 @@ BTAS_D bool bits_differ(T a, T b) {
   else return __builtin_bit_cast(unsigned long long, a) != __builtin_bit_cast(unsigned long long, b);
 }
 
+// two adjacent elements as one 8-byte (4-byte T) or 16-byte (8-byte T) access
+template <class T>
+BTAS_D bool aligned2(const T* p, int64_t ld) {
+  return (ld % 2) == 0 && (reinterpret_cast<uintptr_t>(p) % (2 * sizeof(T))) == 0;
+}
+template <class T>
+BTAS_D void ld2(const T* p, T out[2]) {
+  if constexpr (sizeof(T) == 4) {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    out[0] = __builtin_bit_cast(T, u.x);
+    out[1] = __builtin_bit_cast(T, u.y);
+  } else {
+    const ulonglong2 u = *reinterpret_cast<const ulonglong2*>(p);
+    out[0] = __builtin_bit_cast(T, u.x);
+    out[1] = __builtin_bit_cast(T, u.y);
+  }
+}
+template <class T>
+BTAS_D void st2(T* p, const T v[2]) {
+  if constexpr (sizeof(T) == 4) {
+    *reinterpret_cast<uint2*>(p) = make_uint2(__builtin_bit_cast(uint32_t, v[0]), __builtin_bit_cast(uint32_t, v[1]));
+  } else {
+    ulonglong2 u;
+    u.x = __builtin_bit_cast(unsigned long long, v[0]);
+    u.y = __builtin_bit_cast(unsigned long long, v[1]);
+    *reinterpret_cast<ulonglong2*>(p) = u;
+  }
+}
+
 template <class T, bool MIN>
 BTAS_D T combine(T a, T b) {
   if (MIN) return b < a ? b : a;
@@ -379,9 +408,38 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
     }
 
     // ------------------------------ epilogue ------------------------------
+    // Two passes: first every Z / Cprev operand of the tile is loaded into
+    // registers, then results are formed and stored.  C may alias Z
+    // (Floyd-Warshall updates D in place), so loads interleaved with stores
+    // could not be reordered by the compiler and each load's latency would
+    // be exposed; issuing all loads first keeps ~32 in flight per thread.
     Out* C = static_cast<Out*>(g.C);
     const Out* Z = static_cast<const Out*>(g.Z);
     const Out* Cp = static_cast<const Out*>(g.Cprev);
+    const bool vec2 = aligned2(C, g.ldc) && (Z == nullptr || aligned2(Z, g.ldz)) &&
+                      (Cp == nullptr || aligned2(Cp, g.ldcp));
+    const Out* X = Z != nullptr ? Z : Cp;  // the pre-loaded operand
+    const int64_t ldx = Z != nullptr ? g.ldz : g.ldcp;
+    Out xv[GM][2][GN][2];
+    if (X != nullptr) {
+#pragma unroll
+      for (int i = 0; i < GM; ++i)
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int64_t row = (int64_t)mb * BM + i * 32 + ty * 2 + r;
+#pragma unroll
+          for (int j = 0; j < GN; ++j) {
+            const int64_t col0 = (int64_t)nb * BN + j * 32 + tx * 2;
+            if (row < g.M && vec2 && col0 + 1 < g.N) {
+              ld2(X + row * ldx + col0, xv[i][r][j]);
+            } else {
+#pragma unroll
+              for (int c = 0; c < 2; ++c)
+                xv[i][r][j][c] = (row < g.M && col0 + c < g.N) ? X[row * ldx + col0 + c] : (Out)0;
+            }
+          }
+        }
+    }
 #pragma unroll
     for (int i = 0; i < GM; ++i)
 #pragma unroll
@@ -389,17 +447,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
         const int64_t row = (int64_t)mb * BM + i * 32 + ty * 2 + r;
         if (row >= g.M) continue;
 #pragma unroll
-        for (int j = 0; j < GN; ++j)
+        for (int j = 0; j < GN; ++j) {
+          const int64_t col0 = (int64_t)nb * BN + j * 32 + tx * 2;
+          Out v[2];
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
-            const int64_t col = (int64_t)nb * BN + j * 32 + tx * 2 + c;
-            if (col >= g.N) continue;
-            Out v = P::finish(acc[i][r][j][c], g);
-            if (Z != nullptr) v = combine<Out, MIN>(v, Z[row * g.ldz + col]);
-            if (Cp != nullptr) changed |= bits_differ(v, Cp[row * g.ldcp + col]);
-            if (row == col) diag_neg |= (v < (Out)0);
-            C[row * g.ldc + col] = v;
+            v[c] = P::finish(acc[i][r][j][c], g);
+            if (Z != nullptr) v[c] = combine<Out, MIN>(v[c], xv[i][r][j][c]);
           }
+          if (Cp != nullptr && Z == nullptr) {
+            if (col0 < g.N) changed |= bits_differ(v[0], xv[i][r][j][0]);
+            if (col0 + 1 < g.N) changed |= bits_differ(v[1], xv[i][r][j][1]);
+          } else if (Cp != nullptr) {  // both operands given (rare): second operand read inline
+            if (col0 < g.N) changed |= bits_differ(v[0], Cp[row * g.ldcp + col0]);
+            if (col0 + 1 < g.N) changed |= bits_differ(v[1], Cp[row * g.ldcp + col0 + 1]);
+          }
+          if (row == col0) diag_neg |= (v[0] < (Out)0);
+          if (row == col0 + 1 && col0 + 1 < g.N) diag_neg |= (v[1] < (Out)0);
+          if (vec2 && col0 + 1 < g.N) {
+            st2(C + row * g.ldc + col0, v);
+          } else {
+            if (col0 < g.N) C[row * g.ldc + col0] = v[0];
+            if (col0 + 1 < g.N) C[row * g.ldc + col0 + 1] = v[1];
+          }
+        }
       }
   }
   if (__any_sync(0xffffffffu, changed) && lane == 0) atomicOr(&g.flags[BTAS_FLAG_CHANGED], 1);
