@@ -53,7 +53,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", default="gemm", choices=["gemm", "gemm_f32", "gemm_f32_real", "fw", "apsp"])
+    ap.add_argument("--workload", default="gemm",
+                    choices=["gemm", "gemm_f32", "gemm_f32_real", "fw", "apsp", "matvec", "ewadd"])
+    ap.add_argument("--batch", type=int, default=1, help="vectors per matvec (config C5: 1, 2, 4, 8)")
     ap.add_argument("--n", type=int, default=0, help="problem size (default per workload)")
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -180,6 +182,8 @@ def main():
 
     if args.workload in ("fw", "apsp"):
         return apsp_arm(args, rank, world, dev)
+    if args.workload in ("matvec", "ewadd"):
+        return hbm_arm(args, rank, world, dev)
 
     import paper_1701_04733_b200 as bt
     from paper_1701_04733_b200 import _lib
@@ -440,6 +444,64 @@ def apsp_arm(args, rank, world, dev):
            "config": {"workload": f"{args.workload}_n{n}", "graph": "random_graph p=0.5 weights 1..100",
                       "multiplications": mults, "negative_cycle": rep.negative_cycle,
                       "gpairs_per_s": round(pairs / (ms * 1e-3) / 1e9, 1)}}
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    return 0
+
+
+def hbm_arm(args, rank, world, dev):
+    """Config C5: max-plus batched matvec / elementwise ⊕ at n = 65536 (f32,
+    integers in [-1000, 1000], 10 % Infinity), HBM-bound: GB/s vs the
+    measured copy bandwidth of MEASURED_PEAKS.json."""
+    import torch
+
+    import paper_1701_04733_b200 as bt
+    from paper_1701_04733_b200 import matrix as bm
+
+    n = args.n or 65536
+    MAX = bt.SemiringKind.MAX_PLUS
+    g = torch.Generator(device=dev)
+    g.manual_seed(0xC5)
+
+    def make(rows, cols):
+        sym = torch.randint(-1000, 1001, (rows, cols), generator=g, device=dev, dtype=torch.int32).to(torch.float32)
+        sym[torch.rand((rows, cols), generator=g, device=dev) < 0.10] = math.inf
+        return bt.TropicalMatrix(MAX, sym, dtype=torch.float32, device=dev)
+
+    A = make(n, n)
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    if args.workload == "matvec":
+        V = make(args.batch, n)
+        fn = lambda: bt.matvec_batched(A, V)  # noqa: E731
+        nbytes = (n * n + args.batch * n + args.batch * n) * 4
+        wl = f"maxplus_matvec_n{n}_b{args.batch}_f32"
+    else:
+        B = make(n, n)
+        fn = lambda: bt.ew_add(A, B)  # noqa: E731
+        nbytes = 3 * n * n * 4
+        wl = f"maxplus_ewadd_n{n}_f32"
+    for _ in range(max(3, args.warmup)):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(int(dev.index)) as clocks:
+        s.record()
+        for _ in range(args.steps):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / args.steps
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    res = {"metric": f"{wl} GB/s", "value": round(gbs, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+           "warmup": max(3, args.warmup), "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+           "config": {"workload": wl, "n": n, "bytes_per_step": nbytes, "operands": "integers in [-1000,1000], 10% Inf",
+                      "l2": "matrix 17 GB >> L2"},
+           "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
+                        "frac": round(gbs / hbm, 4), "traffic": None,
+                        "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, read+write)"},
+           "clocks": clocks.summary()}
     if rank == 0:
         print(json.dumps(res), flush=True)
     return 0
