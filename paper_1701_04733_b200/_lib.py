@@ -13,7 +13,10 @@ import ctypes
 import threading
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libbtas_cuda.so"
+import os
+
+# BTAS_LIB overrides the library path (A/B measurements of kernel variants)
+LIB_PATH = Path(os.environ.get("BTAS_LIB") or Path(__file__).resolve().parent / "_lib" / "libbtas_cuda.so")
 
 # constants mirrored from include/btas_cuda.h
 F32, I32, F64 = 0, 1, 2

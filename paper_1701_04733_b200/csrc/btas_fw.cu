@@ -450,17 +450,17 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
       g.skip_hi = g16.skip_hi = f.k0 + b;
       int rc;
       if constexpr (CHECKED) {
-        rc = launch_tropical_gemm<MixChecked<T, true>, true>(g, st);
+        rc = launch_gemm_epi<MixChecked<T, true>, true, kEpiAcc>(g, st);
       } else if constexpr (Traits<T>::dtype == BTAS_F64) {
-        rc = launch_tropical_gemm<MixF64<true>, true>(g, st);
+        rc = launch_gemm_epi<MixF64<true>, true, kEpiAcc>(g, st);
       } else if constexpr (Traits<T>::dtype == BTAS_I32) {
-        rc = launch_tropical_gemm<MixI32<true>, true>(g, st);
+        rc = launch_gemm_epi<MixI32<true>, true, kEpiAcc>(g, st);
       } else {
-        rc = launch_tropical_gemm<MixF32<true>, true>(g, st);
+        rc = launch_gemm_epi<MixF32<true>, true, kEpiAcc>(g, st);
       }
       if (rc) return rc;
       if (emit_s16) {
-        rc = launch_tropical_gemm<MixS16<true, T>, true>(g16, st);
+        rc = launch_gemm_epi<MixS16<true, T>, true, kEpiAcc>(g16, st);
         if (rc) return rc;
       }
     }

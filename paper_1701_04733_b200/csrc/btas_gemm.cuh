@@ -296,7 +296,13 @@ struct GemmShape {
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
-template <class P, bool MIN>
+// EPI (compile-time epilogue operands): bit 0 = accumulate_into Z present,
+// bit 1 = fixpoint reference Cprev present.  Separate instantiations keep the
+// plain product's epilogue minimal (measured: a generic epilogue costs the
+// n = 16384 GEMM ~1 %, profiles/r01_experiments.md).
+enum { kEpiPlain = 0, kEpiAcc = 1, kEpiCmp = 2, kEpiBoth = 3 };
+
+template <class P, bool MIN, int EPI>
 __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __grid_constant__ GemmArgs g) {
   if (g.gate != nullptr && *g.gate != g.gate_value) return;
   using E = typename P::E;
@@ -414,12 +420,49 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
     // could not be reordered by the compiler and each load's latency would
     // be exposed; issuing all loads first keeps ~32 in flight per thread.
     Out* C = static_cast<Out*>(g.C);
-    const Out* Z = static_cast<const Out*>(g.Z);
-    const Out* Cp = static_cast<const Out*>(g.Cprev);
+    const Out* Z = (EPI & kEpiAcc) ? static_cast<const Out*>(g.Z) : nullptr;
+    const Out* Cp = (EPI & kEpiCmp) ? static_cast<const Out*>(g.Cprev) : nullptr;
     const bool vec2 = aligned2(C, g.ldc) && (Z == nullptr || aligned2(Z, g.ldz)) &&
                       (Cp == nullptr || aligned2(Cp, g.ldcp));
     const Out* X = Z != nullptr ? Z : Cp;  // the pre-loaded operand
     const int64_t ldx = Z != nullptr ? g.ldz : g.ldcp;
+    // interior tiles (every tile but the last row/column of tiles): no bounds
+    // tests, all accesses 8/16-byte, diagonal test only on diagonal tiles —
+    // a short straight-line epilogue keeps the instruction cache warm when
+    // K is small (Floyd-Warshall phase 3 runs it every 2-4 k-stages)
+    if (vec2 && (int64_t)(mb + 1) * BM <= g.M && (int64_t)(nb + 1) * BN <= g.N && !(Z != nullptr && Cp != nullptr)) {
+      const int64_t rb = (int64_t)mb * BM + ty * 2, cb = (int64_t)nb * BN + tx * 2;
+      const bool diag_tile = (int64_t)mb * BM < (int64_t)(nb + 1) * BN && (int64_t)nb * BN < (int64_t)(mb + 1) * BM;
+      Out xi[GM][2][GN][2];
+      if (X != nullptr) {
+#pragma unroll
+        for (int i = 0; i < GM; ++i)
+#pragma unroll
+          for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int j = 0; j < GN; ++j) ld2(X + (rb + i * 32 + r) * ldx + cb + j * 32, xi[i][r][j]);
+      }
+#pragma unroll
+      for (int i = 0; i < GM; ++i)
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int64_t row = rb + i * 32 + r;
+#pragma unroll
+          for (int j = 0; j < GN; ++j) {
+            const int64_t col0 = cb + j * 32;
+            Out v[2];
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              v[c] = P::finish(acc[i][r][j][c], g);
+              if (Z != nullptr) v[c] = combine<Out, MIN>(v[c], xi[i][r][j][c]);
+            }
+            if (Cp != nullptr) changed |= bits_differ(v[0], xi[i][r][j][0]) | bits_differ(v[1], xi[i][r][j][1]);
+            if (diag_tile) diag_neg |= (row == col0 && v[0] < (Out)0) | (row == col0 + 1 && v[1] < (Out)0);
+            st2(C + row * g.ldc + col0, v);
+          }
+        }
+      continue;
+    }
     Out xv[GM][2][GN][2];
     if (X != nullptr) {
 #pragma unroll
@@ -483,12 +526,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
 // host-side launcher for one policy
 int device_sm_count();
 
-template <class P, bool MIN>
-int launch_tropical_gemm(const GemmArgs& g, cudaStream_t stream) {
+template <class P, bool MIN, int EPI>
+int launch_gemm_epi(const GemmArgs& g, cudaStream_t stream) {
   using S = GemmShape<P>;
   static bool configured = false;
   if (!configured) {
-    if (cudaFuncSetAttribute(tropical_gemm_kernel<P, MIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(tropical_gemm_kernel<P, MIN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)S::smem_bytes) != cudaSuccess) {
       (void)cudaGetLastError();
       return BTAS_ERR_CUDA;
@@ -498,9 +541,23 @@ int launch_tropical_gemm(const GemmArgs& g, cudaStream_t stream) {
   const int ntiles = g.mblocks * g.nblocks;
   const int grid = ntiles < device_sm_count() ? ntiles : device_sm_count();
   if (grid <= 0) return BTAS_OK;
-  tropical_gemm_kernel<P, MIN><<<grid, kGemmThreads, S::smem_bytes, stream>>>(g);
+  tropical_gemm_kernel<P, MIN, EPI><<<grid, kGemmThreads, S::smem_bytes, stream>>>(g);
   BTAS_CUDA_CHECK_LAUNCH();
   return BTAS_OK;
+}
+
+template <class P, bool MIN>
+int launch_tropical_gemm(const GemmArgs& g, cudaStream_t stream) {
+  switch ((g.Z != nullptr ? kEpiAcc : 0) | (g.Cprev != nullptr ? kEpiCmp : 0)) {
+    case kEpiPlain:
+      return launch_gemm_epi<P, MIN, kEpiPlain>(g, stream);
+    case kEpiAcc:
+      return launch_gemm_epi<P, MIN, kEpiAcc>(g, stream);
+    case kEpiCmp:
+      return launch_gemm_epi<P, MIN, kEpiCmp>(g, stream);
+    default:
+      return launch_gemm_epi<P, MIN, kEpiBoth>(g, stream);
+  }
 }
 
 // packed-layout index: P[blk][kp][r][2]

@@ -71,7 +71,7 @@ def test_partition():
 def test_sharded_squaring_gloo_world2():
     world = 2
     port = _free_port()
-    manager = mp.Manager()
+    manager = mp.get_context("spawn").Manager()
     results = manager.dict()
     mp.spawn(_worker, args=(world, port, results), nprocs=world, join=True)
     for idx, adj in enumerate(_cases()):
