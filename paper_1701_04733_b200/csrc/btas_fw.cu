@@ -28,8 +28,10 @@ namespace btas {
 namespace {
 
 struct FwCtrl {
-  int32_t s16_overflow;  // this round's snapshots leave the s16 domain
-  int32_t pad[63];
+  // snapshots of a pivot block left the s16 domain: [0]/[1] per block
+  // parity, [2] for the pair of blocks merged into one phase-3 pass
+  int32_t s16_overflow[3];
+  int32_t pad[61];
 };
 
 // ------------------------------------------------------------------ rounds
@@ -95,8 +97,10 @@ struct FwArgs {
   int int_mode;
   double limit;
   int BMa, BNb;      // packed block sizes of the 32/64-bit GEMM operands
-  int64_t Kp2;       // b / 2
-  int64_t Kp2w;      // b / 4 (s16 word pairs)
+  int64_t Kp2;       // k-pair stride of the packed panels (capacity: two pivot blocks = b)
+  int64_t Kp2w;      // word-pair stride of the s16 panels (b / 2)
+  int koff;          // k offset of this pivot block inside the panels (0 or b)
+  int parity;        // which s16 flag this block reports to
   int emit_s16;      // also emit the int16x2 operands
   int32_t* flags;
   FwCtrl* ctrl;
@@ -148,7 +152,7 @@ BTAS_D bool emit_history(const T* __restrict__ h, int64_t rc0, int BLK, const Fw
   for (int e = threadIdx.x; e < (b / 2) * b; e += blockDim.x) {
     const int kp = e / b, x = e - kp * b;
     const T v0 = h[(2 * kp) * b + x], v1 = h[(2 * kp + 1) * b + x];
-    const int64_t idx = packed_index(rc0 + x, 2 * kp, f.Kp2, BLK);
+    const int64_t idx = packed_index(rc0 + x, f.koff + 2 * kp, f.Kp2, BLK);
     P[idx] = v0;
     P[idx + 1] = v1;
     out16 |= !s16_ok(v0) || !s16_ok(v1);
@@ -159,7 +163,7 @@ BTAS_D bool emit_history(const T* __restrict__ h, int64_t rc0, int BLK, const Fw
       const int k = 4 * wp;
       const uint32_t w0 = s16_lane(h[k * b + x]) | (s16_lane(h[(k + 1) * b + x]) << 16);
       const uint32_t w1 = s16_lane(h[(k + 2) * b + x]) | (s16_lane(h[(k + 3) * b + x]) << 16);
-      const int64_t idx = packed_index(rc0 + x, 2 * wp, f.Kp2w, 128);
+      const int64_t idx = packed_index(rc0 + x, f.koff / 2 + 2 * wp, f.Kp2w, 128);
       P16[idx] = w0;
       P16[idx + 1] = w1;
     }
@@ -179,7 +183,10 @@ __global__ void __launch_bounds__(kFwThreads) fw_phase1_kernel(T* __restrict__ D
   T* rs = reinterpret_cast<T*>(smem_raw);
   T* cT = rs + b * b;
   const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
-  if (threadIdx.x == 0) f.ctrl->s16_overflow = 0;
+  if (threadIdx.x == 0) {
+    f.ctrl->s16_overflow[f.parity] = 0;
+    if (f.parity == 0) f.ctrl->s16_overflow[2] = 0;
+  }
   T v[R][R];
   load_block(D, f, f.k0, f.k0, ty, tx, v);
   bool sat = false;
@@ -217,7 +224,10 @@ __global__ void __launch_bounds__(kFwThreads) fw_phase1_kernel(T* __restrict__ D
   // pivot rows of Scol (A operand) and pivot columns of Srow (B operand)
   bool out16 = emit_history(cT, f.k0, f.BMa, f, Scol, Scol16);
   out16 |= emit_history(rs, f.k0, f.BNb, f, Srow, Srow16);
-  if (__syncthreads_or(out16) && threadIdx.x == 0) atomicOr(&f.ctrl->s16_overflow, 1);
+  if (__syncthreads_or(out16) && threadIdx.x == 0) {
+    atomicOr(&f.ctrl->s16_overflow[f.parity], 1);
+    atomicOr(&f.ctrl->s16_overflow[2], 1);
+  }
   if (MODE == kChecked && __any_sync(0xffffffffu, sat) && (threadIdx.x & 31) == 0)
     atomicOr(&f.flags[BTAS_FLAG_SATURATED], 1);
 }
@@ -282,7 +292,10 @@ __global__ void __launch_bounds__(kFwThreads) fw_phase2_kernel(T* __restrict__ D
   __syncthreads();
   const bool out16 = row_panel ? emit_history(hist, c0, f.BNb, f, Srow, Srow16)
                                : emit_history(hist, r0, f.BMa, f, Scol, Scol16);
-  if (__syncthreads_or(out16) && threadIdx.x == 0) atomicOr(&f.ctrl->s16_overflow, 1);
+  if (__syncthreads_or(out16) && threadIdx.x == 0) {
+    atomicOr(&f.ctrl->s16_overflow[f.parity], 1);
+    atomicOr(&f.ctrl->s16_overflow[2], 1);
+  }
   if (MODE == kChecked && __any_sync(0xffffffffu, sat) && (threadIdx.x & 31) == 0)
     atomicOr(&f.flags[BTAS_FLAG_SATURATED], 1);
 }
@@ -340,13 +353,13 @@ FwWs fw_ws(int64_t n) {
   w.csp = off;
   off += a256((size_t)G::b * G::b * sizeof(T));
   w.scol = off;
-  off += a256((size_t)rows * G::b * sizeof(T));
+  off += a256((size_t)rows * 2 * G::b * sizeof(T));  // two pivot blocks of k
   w.srow = off;
-  off += a256((size_t)cols * G::b * sizeof(T));
+  off += a256((size_t)cols * 2 * G::b * sizeof(T));
   w.scol16 = off;
-  off += a256((size_t)rows * (G::b / 2) * 4);
+  off += a256((size_t)rows * G::b * 4);
   w.srow16 = off;
-  off += a256((size_t)cols * (G::b / 2) * 4);
+  off += a256((size_t)cols * G::b * 4);
   w.total = off;
   return w;
 }
@@ -388,8 +401,8 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
   f.limit = limit;
   f.BMa = G::BMa;
   f.BNb = G::BNb;
-  f.Kp2 = b / 2;
-  f.Kp2w = b / 4;
+  f.Kp2 = b;       // panels hold two pivot blocks: 2b k values = b k-pairs
+  f.Kp2w = b / 2;  // 2b k values = b words = b/2 word pairs
   f.emit_s16 = emit_s16 ? 1 : 0;
   f.flags = flags;
   f.ctrl = ctrl;
@@ -408,10 +421,13 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
     configured = true;
   }
 
+  // base GEMM descriptors over the full D; per launch only the k range
+  // (which half of the panels), the row/col window and the skip ranges change
   GemmArgs g{};
   g.Ap = scol;
   g.Bp = srow;
   g.Kp2 = b / 2;
+  g.Kp2s = b;
   g.M = n;
   g.N = n;
   g.mblocks = (int)(rows / G::BMa);
@@ -424,45 +440,107 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
   g.flags = flags;
   g.integer_mode = int_mode ? 1 : 0;
   g.limit = int_mode ? limit : INFINITY;
-  g.gate = emit_s16 ? &ctrl->s16_overflow : nullptr;
   g.gate_value = 1;
-
+  g.no_diag = 1;  // windows below offset C; FW tests the diagonal once at the end
   GemmArgs g16 = g;
   g16.Ap = scol16;
   g16.Bp = srow16;
   g16.Kp2 = b / 4;
+  g16.Kp2s = b / 2;
   g16.mblocks = (int)(round_up(rows, 128) / 128);
   g16.nblocks = (int)(round_up(cols, 128) / 128);
-  g16.gate = &ctrl->s16_overflow;
   g16.gate_value = 0;
   g16.limit = limit;
   g16.integer_mode = 1;
 
-  for (int kb = 0; kb < nblk; ++kb) {
-    f.k0 = (int64_t)kb * b;
-    fw_phase1_kernel<T, MODE><<<1, kFwThreads, smem1, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
-    if (nblk > 1) {
-      fw_phase2_kernel<T, MODE><<<dim3(nblk, 2), kFwThreads, smem2, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
+  // one phase-3 style update: 32-bit kernel gated on "s16 overflow", s16x2
+  // kernel gated on "no overflow" (flag word `fl`); half = first k half used,
+  // halves = 1 (K = b) or 2 (K = 2b, two pivot blocks merged)
+  auto phase3 = [&](GemmArgs a, GemmArgs a16, int fl, int half, int halves) -> int {
+    a.Kp2 = (int64_t)halves * b / 2;
+    a16.Kp2 = (int64_t)halves * b / 4;
+    a.Ap = static_cast<const T*>(a.Ap) + (size_t)half * (b / 2) * G::BMa * 2;
+    a.Bp = static_cast<const T*>(a.Bp) + (size_t)half * (b / 2) * G::BNb * 2;
+    a16.Ap = static_cast<const uint32_t*>(a16.Ap) + (size_t)half * (b / 4) * 128 * 2;
+    a16.Bp = static_cast<const uint32_t*>(a16.Bp) + (size_t)half * (b / 4) * 128 * 2;
+    a.gate = emit_s16 ? &ctrl->s16_overflow[fl] : nullptr;
+    a16.gate = &ctrl->s16_overflow[fl];
+    int rc;
+    if constexpr (CHECKED) {
+      rc = launch_gemm_epi<MixChecked<T, true>, true, kEpiAcc>(a, st);
+    } else if constexpr (Traits<T>::dtype == BTAS_F64) {
+      rc = launch_gemm_epi<MixF64<true>, true, kEpiAcc>(a, st);
+    } else if constexpr (Traits<T>::dtype == BTAS_I32) {
+      rc = launch_gemm_epi<MixI32<true>, true, kEpiAcc>(a, st);
+    } else {
+      rc = launch_gemm_epi<MixF32<true>, true, kEpiAcc>(a, st);
     }
+    if (rc) return rc;
+    if (emit_s16) rc = launch_gemm_epi<MixS16<true, T>, true, kEpiAcc>(a16, st);
+    return rc;
+  };
+  auto phases12 = [&](int kb) -> int {
+    f.k0 = (int64_t)kb * b;
+    f.parity = kb & 1;
+    f.koff = (kb & 1) * b;
+    fw_phase1_kernel<T, MODE><<<1, kFwThreads, smem1, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
+    if (nblk > 1)
+      fw_phase2_kernel<T, MODE><<<dim3(nblk, 2), kFwThreads, smem2, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
     BTAS_CUDA_CHECK_LAUNCH();
-    if (nblk > 1) {
-      g.skip_lo = g16.skip_lo = f.k0;
-      g.skip_hi = g16.skip_hi = f.k0 + b;
-      int rc;
-      if constexpr (CHECKED) {
-        rc = launch_gemm_epi<MixChecked<T, true>, true, kEpiAcc>(g, st);
-      } else if constexpr (Traits<T>::dtype == BTAS_F64) {
-        rc = launch_gemm_epi<MixF64<true>, true, kEpiAcc>(g, st);
-      } else if constexpr (Traits<T>::dtype == BTAS_I32) {
-        rc = launch_gemm_epi<MixI32<true>, true, kEpiAcc>(g, st);
-      } else {
-        rc = launch_gemm_epi<MixF32<true>, true, kEpiAcc>(g, st);
-      }
-      if (rc) return rc;
-      if (emit_s16) {
-        rc = launch_gemm_epi<MixS16<true, T>, true, kEpiAcc>(g16, st);
-        if (rc) return rc;
-      }
+    return BTAS_OK;
+  };
+
+  // Lookahead by one pivot block (4-byte storage; b == the GEMM tile edge):
+  // block kb's phase-3 update is applied right away only to the row and
+  // column panels of block kb+1 (which block kb+1's phases 1/2 read), and
+  // for every other tile it is merged with block kb+1's update into ONE
+  // K = 2b pass.  Candidates are formed from the same snapshots either way
+  // and min is order-free, so D is unchanged; the bulk pass does twice the
+  // add-min work per epilogue (tile load + store of D).
+  constexpr bool kLookahead = sizeof(T) == 4;
+  int rc;
+  for (int kb = 0; kb < nblk; kb += kLookahead ? 2 : 1) {
+    if ((rc = phases12(kb))) return rc;
+    if (nblk == 1) break;
+    const int64_t k0 = (int64_t)kb * b;
+    if (!kLookahead || kb + 1 == nblk) {
+      GemmArgs a = g, a16 = g16;
+      a.skip_row_lo = a16.skip_row_lo = a.skip_col_lo = a16.skip_col_lo = k0;
+      a.skip_row_hi = a16.skip_row_hi = a.skip_col_hi = a16.skip_col_hi = k0 + b;
+      if ((rc = phase3(a, a16, kb & 1, kb & 1, 1))) return rc;
+      continue;
+    }
+    const int64_t k1 = k0 + b, m1 = std::min<int64_t>(b, n - k1);
+    {  // (a) block kb -> row panel of kb+1 (all columns except block kb)
+      GemmArgs a = g, a16 = g16;
+      a.M = a16.M = m1;
+      a.mblocks = a16.mblocks = 1;
+      a.Ap = static_cast<const T*>(g.Ap) + (size_t)(kb + 1) * g.Kp2s * G::BMa * 2;
+      a16.Ap = static_cast<const uint32_t*>(g16.Ap) + (size_t)(kb + 1) * g16.Kp2s * 128 * 2;
+      a.C = a16.C = D + k1 * ld;
+      a.Z = a16.Z = D + k1 * ld;
+      a.skip_col_lo = a16.skip_col_lo = k0;
+      a.skip_col_hi = a16.skip_col_hi = k0 + b;
+      if ((rc = phase3(a, a16, 0, 0, 1))) return rc;
+    }
+    {  // (b) block kb -> column panel of kb+1 (all rows except blocks kb, kb+1)
+      GemmArgs a = g, a16 = g16;
+      a.N = a16.N = m1;
+      a.nblocks = a16.nblocks = 1;
+      a.Bp = static_cast<const T*>(g.Bp) + (size_t)(kb + 1) * g.Kp2s * G::BNb * 2;
+      a16.Bp = static_cast<const uint32_t*>(g16.Bp) + (size_t)(kb + 1) * g16.Kp2s * 128 * 2;
+      a.C = a16.C = D + k1;
+      a.Z = a16.Z = D + k1;
+      a.skip_row_lo = a16.skip_row_lo = k0;
+      a.skip_row_hi = a16.skip_row_hi = k1 + b;
+      if ((rc = phase3(a, a16, 0, 0, 1))) return rc;
+    }
+    if ((rc = phases12(kb + 1))) return rc;
+    {  // (c) blocks kb and kb+1 together on every tile outside row/col block kb+1
+      GemmArgs a = g, a16 = g16;
+      a.skip_row_lo = a16.skip_row_lo = a.skip_col_lo = a16.skip_col_lo = k1;
+      a.skip_row_hi = a16.skip_row_hi = a.skip_col_hi = a16.skip_col_hi = k1 + b;
+      if ((rc = phase3(a, a16, 2, 0, 2))) return rc;
     }
   }
   return BTAS_OK;

@@ -53,7 +53,11 @@ struct GemmArgs {
   int32_t* flags;        // BTAS_NUM_FLAGS device ints
   const int32_t* gate;   // nullable: run only when *gate == gate_value
   int gate_value;
-  int64_t skip_lo, skip_hi;  // skip tiles whose rows or cols lie inside [lo, hi)
+  // skip tiles whose rows lie inside [skip_row_lo, skip_row_hi) or whose
+  // cols lie inside [skip_col_lo, skip_col_hi) (empty ranges: no skipping)
+  int64_t skip_row_lo, skip_row_hi, skip_col_lo, skip_col_hi;
+  int64_t Kp2s;          // k-pair stride between blocks of the packed buffers (0: = Kp2)
+  int no_diag;           // 1: skip the diag<0 test (C is a window, not the whole matrix)
   int integer_mode;
   double limit;          // saturation limit (integer limit, or +inf for float mode)
 };
@@ -333,9 +337,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
   const int nkb = (int)(g.Kp2 / KP);
 
   auto skipped = [&](int mb, int nb) {
-    if (g.skip_hi <= g.skip_lo) return false;
     const int64_t r0 = (int64_t)mb * BM, c0 = (int64_t)nb * BN;
-    return (r0 >= g.skip_lo && r0 + BM <= g.skip_hi) || (c0 >= g.skip_lo && c0 + BN <= g.skip_hi);
+    return (r0 >= g.skip_row_lo && r0 + BM <= g.skip_row_hi) || (c0 >= g.skip_col_lo && c0 + BN <= g.skip_col_hi);
   };
 
   // ------------------------------ producer --------------------------------
@@ -351,8 +354,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
         int mb, nb;
         tile_coords(tile, g.mblocks, g.nblocks, mb, nb);
         if (skipped(mb, nb)) continue;
-        const E* gA = static_cast<const E*>(g.Ap) + (size_t)mb * g.Kp2 * BM * 2;
-        const E* gB = static_cast<const E*>(g.Bp) + (size_t)nb * g.Kp2 * BN * 2;
+        const int64_t kps = g.Kp2s ? g.Kp2s : g.Kp2;
+        const E* gA = static_cast<const E*>(g.Ap) + (size_t)mb * kps * BM * 2;
+        const E* gB = static_cast<const E*>(g.Bp) + (size_t)nb * kps * BN * 2;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % ST;
           if (it >= (uint32_t)ST) mbar_wait(&empty[s], ((it / ST) - 1) & 1);
@@ -376,6 +380,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
     int mb, nb;
     tile_coords(tile, g.mblocks, g.nblocks, mb, nb);
     if (skipped(mb, nb)) continue;
+
+    // epilogue operands: for interior tiles the Z / Cprev values are loaded
+    // BEFORE the k loop, so their latency hides behind the add-min work
+    Out* C = static_cast<Out*>(g.C);
+    const Out* Z = (EPI & kEpiAcc) ? static_cast<const Out*>(g.Z) : nullptr;
+    const Out* Cp = (EPI & kEpiCmp) ? static_cast<const Out*>(g.Cprev) : nullptr;
+    const bool vec2 = aligned2(C, g.ldc) && (Z == nullptr || aligned2(Z, g.ldz)) &&
+                      (Cp == nullptr || aligned2(Cp, g.ldcp));
+    const Out* X = Z != nullptr ? Z : Cp;  // the pre-loaded operand
+    const int64_t ldx = Z != nullptr ? g.ldz : g.ldcp;
+    const bool interior = vec2 && (int64_t)(mb + 1) * BM <= g.M && (int64_t)(nb + 1) * BN <= g.N &&
+                          !(Z != nullptr && Cp != nullptr);
+    const int64_t rb = (int64_t)mb * BM + ty * 2, cb = (int64_t)nb * BN + tx * 2;
+    Out xi[GM][2][GN][2];
+    if (interior && X != nullptr) {
+#pragma unroll
+      for (int i = 0; i < GM; ++i)
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int j = 0; j < GN; ++j) ld2(X + (rb + i * 32 + r) * ldx + cb + j * 32, xi[i][r][j]);
+    }
 
     Acc acc[GM][2][GN][2];
 #pragma unroll
@@ -414,34 +440,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
     }
 
     // ------------------------------ epilogue ------------------------------
-    // Two passes: first every Z / Cprev operand of the tile is loaded into
-    // registers, then results are formed and stored.  C may alias Z
-    // (Floyd-Warshall updates D in place), so loads interleaved with stores
-    // could not be reordered by the compiler and each load's latency would
-    // be exposed; issuing all loads first keeps ~32 in flight per thread.
-    Out* C = static_cast<Out*>(g.C);
-    const Out* Z = (EPI & kEpiAcc) ? static_cast<const Out*>(g.Z) : nullptr;
-    const Out* Cp = (EPI & kEpiCmp) ? static_cast<const Out*>(g.Cprev) : nullptr;
-    const bool vec2 = aligned2(C, g.ldc) && (Z == nullptr || aligned2(Z, g.ldz)) &&
-                      (Cp == nullptr || aligned2(Cp, g.ldcp));
-    const Out* X = Z != nullptr ? Z : Cp;  // the pre-loaded operand
-    const int64_t ldx = Z != nullptr ? g.ldz : g.ldcp;
-    // interior tiles (every tile but the last row/column of tiles): no bounds
-    // tests, all accesses 8/16-byte, diagonal test only on diagonal tiles —
-    // a short straight-line epilogue keeps the instruction cache warm when
-    // K is small (Floyd-Warshall phase 3 runs it every 2-4 k-stages)
-    if (vec2 && (int64_t)(mb + 1) * BM <= g.M && (int64_t)(nb + 1) * BN <= g.N && !(Z != nullptr && Cp != nullptr)) {
-      const int64_t rb = (int64_t)mb * BM + ty * 2, cb = (int64_t)nb * BN + tx * 2;
-      const bool diag_tile = (int64_t)mb * BM < (int64_t)(nb + 1) * BN && (int64_t)nb * BN < (int64_t)(mb + 1) * BM;
-      Out xi[GM][2][GN][2];
-      if (X != nullptr) {
-#pragma unroll
-        for (int i = 0; i < GM; ++i)
-#pragma unroll
-          for (int r = 0; r < 2; ++r)
-#pragma unroll
-            for (int j = 0; j < GN; ++j) ld2(X + (rb + i * 32 + r) * ldx + cb + j * 32, xi[i][r][j]);
-      }
+    // Interior tiles (every tile but the last row/column of tiles): operands
+    // already in registers, no bounds tests, 8/16-byte stores, diagonal test
+    // only on diagonal tiles.  Edge tiles: two passes (all loads, then all
+    // stores — C may alias Z in Floyd-Warshall, so interleaving them would
+    // serialise each load's latency).
+    if (interior) {
+      const bool diag_tile = !g.no_diag && (int64_t)mb * BM < (int64_t)(nb + 1) * BN &&
+                             (int64_t)nb * BN < (int64_t)(mb + 1) * BM;
 #pragma unroll
       for (int i = 0; i < GM; ++i)
 #pragma unroll
@@ -505,8 +511,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
             if (col0 < g.N) changed |= bits_differ(v[0], Cp[row * g.ldcp + col0]);
             if (col0 + 1 < g.N) changed |= bits_differ(v[1], Cp[row * g.ldcp + col0 + 1]);
           }
-          if (row == col0) diag_neg |= (v[0] < (Out)0);
-          if (row == col0 + 1 && col0 + 1 < g.N) diag_neg |= (v[1] < (Out)0);
+          if (!g.no_diag) {
+            if (row == col0) diag_neg |= (v[0] < (Out)0);
+            if (row == col0 + 1 && col0 + 1 < g.N) diag_neg |= (v[1] < (Out)0);
+          }
           if (vec2 && col0 + 1 < g.N) {
             st2(C + row * g.ldc + col0, v);
           } else {

@@ -348,7 +348,6 @@ int gemm_typed(int integer_mode, const T* A, int64_t lda, const T* B, int64_t ld
     g.gate = &ctrl->path;
     g.integer_mode = int_mode ? 1 : 0;
     g.limit = int_mode ? limit : INFINITY;
-    g.skip_lo = g.skip_hi = 0;
   }
   GemmArgs g16{};  // int16x2 path (integer operands with |x| < 2^12)
   const int bn16 = 32 * s16_gn();
