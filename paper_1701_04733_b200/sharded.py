@@ -42,6 +42,27 @@ class ShardedResult:
     saturated: bool
 
 
+def apsp_by_squaring_distributed(adj, group=None):
+    """``apsp_by_squaring`` (reference apsp.py:136-178) row-sharded over the
+    ranks of ``group`` (one process per GPU, NCCL).  Every rank passes the
+    same adjacency matrix and receives the full ApspReport; distances,
+    multiplication count and negative-cycle flag equal the single-GPU
+    result byte for byte."""
+    from .apsp import Algorithm, ApspReport, DistanceMatrix, _closure_base, _require_square_minplus
+    from .matrix import TropicalMatrix
+    from .semiring import _note_saturation
+
+    n = _require_square_minplus(adj)
+    base = _closure_base(adj)
+    res = apsp_by_squaring_sharded(base.data.contiguous(), group=group,
+                                   gemm_rows=_cuda_gemm_rows(True, base.integer), integer=base.integer)
+    if res.saturated:
+        _note_saturation()
+    dist_m = TropicalMatrix._wrap(adj.kind, res.distances.contiguous(), base.integer)
+    return ApspReport(distances=DistanceMatrix(n, dist_m), algorithm=Algorithm.REPEATED_SQUARING,
+                      negative_cycle=res.negative_cycle, multiplications_performed=res.multiplications_performed)
+
+
 def partition(n: int, world: int, align: int = 128) -> "tuple[int, list[tuple[int, int]]]":
     """Equal, tile-aligned row chunks: returns (chunk, [(r0, r1) per rank]).
     Ranks past the end get empty ranges."""

@@ -194,3 +194,29 @@ def test_input_errors(cuda):
         bt.DistanceMatrix(2, bt.TropicalMatrix(MAX, [[0, 1], [1, 0]]))
     with pytest.raises(bt.DimensionMismatch):
         bt.DistanceMatrix(3, bt.identity_matrix(MIN, 2))
+
+
+def test_sharded_squaring_nccl_single_rank(cuda):
+    """The distributed squaring path (NCCL all-gather + flag all-reduce, CUDA
+    row-block GEMM) on a one-rank group: identical to apsp_by_squaring."""
+    import torch.distributed as dist
+
+    from paper_1701_04733_b200.sharded import apsp_by_squaring_distributed
+
+    created = False
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", store=dist.HashStore(), rank=0, world_size=1, device_id=cuda)
+        created = True
+    try:
+        for n, p, wr, seed, dtype in ((300, 0.5, (1, 100), 31, torch.int32), (700, 0.05, (1, 50), 32, torch.float32),
+                                      (129, 0.4, (-3, 10), 33, torch.float64), (1, 0.5, (1, 5), 34, torch.int32)):
+            adj = random_graph_matrix(n, p, wr, seed, dtype=dtype)
+            want = bt.apsp_by_squaring(adj)
+            got = apsp_by_squaring_distributed(adj)
+            assert got.negative_cycle == want.negative_cycle
+            assert got.multiplications_performed == want.multiplications_performed
+            if not want.negative_cycle:
+                assert got.distances.dist == want.distances.dist
+    finally:
+        if created:
+            dist.destroy_process_group()
