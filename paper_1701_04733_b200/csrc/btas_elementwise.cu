@@ -3,6 +3,7 @@
 // All are grid-stride, 16-byte vectorised where alignment allows, and sized
 // to a multiple of the SM count.
 #include <algorithm>
+#include <type_traits>
 
 #include "btas_common.cuh"
 
@@ -18,23 +19,28 @@ inline unsigned grid_for(int64_t work, int threads = 256) {
 }
 
 // ------------------------------------------------------------------ stats
+// Per-thread statistics in the narrowest exact arithmetic A (float for f32
+// data: B200 FP64 is a slow pipe), 32-bit per-thread counters, folded into
+// the 64-bit device struct once per warp.
+template <class A>
 struct LocalStats {
-  unsigned long long nan = 0, neg_inf = 0, non_integral = 0, over = 0, out_of_range = 0, finite = 0;
-  double max_abs = -1.0;  // < 0: none
-  double mn = INFINITY, mx = -INFINITY;
+  uint32_t nan = 0, neg_inf = 0, non_integral = 0, over = 0, out_of_range = 0, finite = 0;
+  A max_abs = (A)-1;  // < 0: none
+  A mn = (A)INFINITY, mx = (A)-INFINITY;
 
-  BTAS_D void add_finite(double v, double int_limit) {
+  BTAS_D void add_finite(A v, A int_limit) {
     finite++;
     if (v != floor(v)) non_integral++;
-    const double a = fabs(v);
+    const A a = fabs(v);
     if (a >= int_limit) over++;
-    max_abs = fmax(max_abs, a);
-    mn = fmin(mn, v);
-    mx = fmax(mx, v);
+    max_abs = a > max_abs ? a : max_abs;
+    mn = v < mn ? v : mn;
+    mx = v > mx ? v : mx;
   }
 };
 
-BTAS_D unsigned long long warp_sum(unsigned long long v) {
+BTAS_D unsigned long long warp_sum(uint32_t v32) {
+  unsigned long long v = v32;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
@@ -51,27 +57,23 @@ BTAS_D double warp_min(double v) {
 }
 
 // warp-aggregated commit: one set of atomics per warp
-BTAS_D void commit(LocalStats s, btas_stats* out) {
-  s.nan = warp_sum(s.nan);
-  s.neg_inf = warp_sum(s.neg_inf);
-  s.non_integral = warp_sum(s.non_integral);
-  s.over = warp_sum(s.over);
-  s.out_of_range = warp_sum(s.out_of_range);
-  s.finite = warp_sum(s.finite);
-  s.max_abs = warp_max(s.max_abs);
-  s.mn = warp_min(s.mn);
-  s.mx = warp_max(s.mx);
+template <class A>
+BTAS_D void commit(const LocalStats<A>& s, btas_stats* out) {
+  const unsigned long long nan = warp_sum(s.nan), neg_inf = warp_sum(s.neg_inf),
+                           non_integral = warp_sum(s.non_integral), over = warp_sum(s.over),
+                           out_of_range = warp_sum(s.out_of_range), finite = warp_sum(s.finite);
+  const double max_abs = warp_max((double)s.max_abs), mn = warp_min((double)s.mn), mx = warp_max((double)s.mx);
   if ((threadIdx.x & 31) != 0) return;
-  if (s.nan) atomicAdd(&out->nan_count, s.nan);
-  if (s.neg_inf) atomicAdd(&out->neg_inf_count, s.neg_inf);
-  if (s.non_integral) atomicAdd(&out->non_integral, s.non_integral);
-  if (s.over) atomicAdd(&out->over_limit, s.over);
-  if (s.out_of_range) atomicAdd(&out->out_of_range, s.out_of_range);
-  if (s.finite) {
-    atomicAdd(&out->finite_count, s.finite);
-    atomicMax(&out->max_abs_key, f64_key(s.max_abs));
-    atomicMin(&out->min_key, f64_key(s.mn));
-    atomicMax(&out->max_key, f64_key(s.mx));
+  if (nan) atomicAdd(&out->nan_count, nan);
+  if (neg_inf) atomicAdd(&out->neg_inf_count, neg_inf);
+  if (non_integral) atomicAdd(&out->non_integral, non_integral);
+  if (over) atomicAdd(&out->over_limit, over);
+  if (out_of_range) atomicAdd(&out->out_of_range, out_of_range);
+  if (finite) {
+    atomicAdd(&out->finite_count, finite);
+    atomicMax(&out->max_abs_key, f64_key(max_abs));
+    atomicMin(&out->min_key, f64_key(mn));
+    atomicMax(&out->max_key, f64_key(mx));
   }
 }
 
@@ -86,35 +88,37 @@ __global__ void stats_init_kernel(btas_stats* s) {
 template <class S, class D>
 __global__ void ingest_kernel(bool min_plus, const S* __restrict__ src, int64_t n, D* __restrict__ dst,
                               btas_stats* stats) {
-  LocalStats st;
+  // statistics arithmetic: float whenever the data is float32 on either side
+  using A = typename std::conditional<sizeof(S) == 4 || Traits<D>::dtype == BTAS_F32, float, double>::type;
+  LocalStats<A> st;
+  const D inf = Traits<D>::eps(min_plus);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double x = (double)src[i];
+    const S x = src[i];
     D out;
-    if (isnan(x)) {
+    if (x != x) {
       st.nan++;
-      out = Traits<D>::eps(min_plus);
-    } else if (x == -INFINITY) {
+      out = inf;
+    } else if (x == (S)-INFINITY) {
       st.neg_inf++;
-      out = Traits<D>::eps(min_plus);
-    } else if (x == INFINITY) {
-      out = Traits<D>::eps(min_plus);  // symbolic Infinity -> oriented (matrix.py:92-94)
+      out = inf;
+    } else if (x == (S)INFINITY) {
+      out = inf;  // symbolic Infinity -> oriented (matrix.py:92-94)
     } else {
-      const double v = x + 0.0;  // -0.0 -> +0.0 (matrix.py:92)
+      const S v = x + (S)0;  // -0.0 -> +0.0 (matrix.py:92)
       if constexpr (Traits<D>::dtype == BTAS_I32) {
-        if (v != floor(v) || fabs(v) >= (double)kI32Limit) {
+        if (v != floor(v) || fabs(v) >= (S)kI32Limit) {
           st.out_of_range++;
           out = 0;
         } else {
           out = (int32_t)v;
         }
-        st.add_finite(v, Traits<D>::int_limit);
+        st.add_finite((A)v, (A)Traits<D>::int_limit);
       } else {
         out = (D)v;
-        const double stored = (double)out;
-        if (isinf(stored)) {
-          st.out_of_range++;
+        if (isinf(out)) {
+          st.out_of_range++;  // finite double beyond the float range
         } else {
-          st.add_finite(stored, Traits<D>::int_limit);
+          st.add_finite((A)out, (A)Traits<D>::int_limit);
         }
       }
     }
@@ -126,16 +130,17 @@ __global__ void ingest_kernel(bool min_plus, const S* __restrict__ src, int64_t 
 // ------------------------------------------------------------------ scan
 template <class T>
 __global__ void scan_kernel(const T* __restrict__ x, int64_t n, btas_stats* stats) {
-  LocalStats st;
+  // int32 magnitudes up to 2^28 need double to stay exact; f32 stays float
+  LocalStats<typename std::conditional<Traits<T>::dtype == BTAS_F32, float, double>::type> st;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const T v = x[i];
     if constexpr (Traits<T>::dtype != BTAS_I32) {
-      if (isnan((double)v)) {
+      if (v != v) {
         st.nan++;
         continue;
       }
     }
-    if (Traits<T>::finite(v)) st.add_finite((double)v, Traits<T>::int_limit);
+    if (Traits<T>::finite(v)) st.add_finite(v, Traits<T>::int_limit);
   }
   commit(st, stats);
 }

@@ -80,6 +80,20 @@ __global__ void init_ws_kernel(Ctrl* ctrl, unsigned long long* extA, unsigned lo
 }
 
 // ------------------------------------------------------------------ extremes
+// Per-k extremes of the finite entries, accumulated in the storage type
+// (B200's FP64 pipe is slow; converting every element to double halved the
+// throughput of these passes) and converted once per thread.
+template <class T>
+BTAS_D T lowest() {
+  if constexpr (Traits<T>::dtype == BTAS_I32) return (T)(-kI32Limit);
+  else return (T)-INFINITY;
+}
+template <class T>
+BTAS_D T highest() {
+  if constexpr (Traits<T>::dtype == BTAS_I32) return (T)kI32Limit;
+  else return (T)INFINITY;
+}
+
 // A (M x K): per column k, max and min over the finite entries of that column.
 template <class T>
 __global__ void ext_cols_kernel(const T* __restrict__ A, int64_t lda, int64_t M, int64_t K, int rows_per_cta,
@@ -88,20 +102,20 @@ __global__ void ext_cols_kernel(const T* __restrict__ A, int64_t lda, int64_t M,
   if (k >= K) return;
   const int64_t r0 = (int64_t)blockIdx.y * rows_per_cta;
   const int64_t r1 = min(M, r0 + rows_per_cta);
-  double mx = -INFINITY, mn = INFINITY;
+  T mx = lowest<T>(), mn = highest<T>();
   bool any = false;
+#pragma unroll 8
   for (int64_t r = r0; r < r1; ++r) {
     const T x = A[r * lda + k];
     if (Traits<T>::finite(x)) {
-      const double d = (double)x;
-      mx = fmax(mx, d);
-      mn = fmin(mn, d);
+      mx = x > mx ? x : mx;
+      mn = x < mn ? x : mn;
       any = true;
     }
   }
   if (any) {
-    atomicMax(&ext[k], f64_key(mx));
-    atomicMin(&ext[K + k], f64_key(mn));
+    atomicMax(&ext[k], f64_key((double)mx));
+    atomicMin(&ext[K + k], f64_key((double)mn));
   }
 }
 
@@ -111,39 +125,42 @@ __global__ void ext_rows_kernel(const T* __restrict__ B, int64_t ldb, int64_t K,
                                 unsigned long long* ext) {
   const int64_t k = blockIdx.x;
   const T* row = B + k * ldb;
-  double mx = -INFINITY, mn = INFINITY;
+  T mx = lowest<T>(), mn = highest<T>();
+  bool any = false;
+#pragma unroll 4
   for (int64_t j = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.y * blockDim.x) {
     const T x = row[j];
     if (Traits<T>::finite(x)) {
-      const double d = (double)x;
-      mx = fmax(mx, d);
-      mn = fmin(mn, d);
+      mx = x > mx ? x : mx;
+      mn = x < mn ? x : mn;
+      any = true;
     }
   }
+  double dmx = any ? (double)mx : -INFINITY, dmn = any ? (double)mn : INFINITY;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    dmx = fmax(dmx, __shfl_xor_sync(0xffffffffu, dmx, o));
+    dmn = fmin(dmn, __shfl_xor_sync(0xffffffffu, dmn, o));
   }
   __shared__ double smx[32], smn[32];
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   if (l == 0) {
-    smx[w] = mx;
-    smn[w] = mn;
+    smx[w] = dmx;
+    smn[w] = dmn;
   }
   __syncthreads();
   if (w == 0) {
     const int nw = blockDim.x >> 5;
-    mx = l < nw ? smx[l] : -INFINITY;
-    mn = l < nw ? smn[l] : INFINITY;
+    dmx = l < nw ? smx[l] : -INFINITY;
+    dmn = l < nw ? smn[l] : INFINITY;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      dmx = fmax(dmx, __shfl_xor_sync(0xffffffffu, dmx, o));
+      dmn = fmin(dmn, __shfl_xor_sync(0xffffffffu, dmn, o));
     }
-    if (l == 0 && mx >= mn) {  // at least one finite entry
-      atomicMax(&ext[k], f64_key(mx));
-      atomicMin(&ext[K + k], f64_key(mn));
+    if (l == 0 && dmx >= dmn) {  // at least one finite entry
+      atomicMax(&ext[k], f64_key(dmx));
+      atomicMin(&ext[K + k], f64_key(dmn));
     }
   }
 }
