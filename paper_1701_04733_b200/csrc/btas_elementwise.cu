@@ -85,6 +85,40 @@ __global__ void stats_init_kernel(btas_stats* s) {
 }
 
 // ------------------------------------------------------------------ ingest
+template <class S, class D, class A>
+BTAS_D D ingest_one(S x, D inf, LocalStats<A>& st) {
+  D out;
+  if (x != x) {
+    st.nan++;
+    out = inf;
+  } else if (x == (S)-INFINITY) {
+    st.neg_inf++;
+    out = inf;
+  } else if (x == (S)INFINITY) {
+    out = inf;  // symbolic Infinity -> oriented (matrix.py:92-94)
+  } else {
+    const S v = x + (S)0;  // -0.0 -> +0.0 (matrix.py:92)
+    if constexpr (Traits<D>::dtype == BTAS_I32) {
+      if (v != floor(v) || fabs(v) >= (S)kI32Limit) {
+        st.out_of_range++;
+        out = 0;
+      } else {
+        out = (int32_t)v;
+      }
+      st.add_finite((A)v, (A)Traits<D>::int_limit);
+    } else {
+      out = (D)v;
+      if (isinf(out)) {
+        st.out_of_range++;  // finite double beyond the float range
+      } else {
+        st.add_finite((A)out, (A)Traits<D>::int_limit);
+      }
+    }
+  }
+  return out;
+}
+
+
 template <class S, class D>
 __global__ void ingest_kernel(bool min_plus, const S* __restrict__ src, int64_t n, D* __restrict__ dst,
                               btas_stats* stats) {
@@ -92,38 +126,17 @@ __global__ void ingest_kernel(bool min_plus, const S* __restrict__ src, int64_t 
   using A = typename std::conditional<sizeof(S) == 4 || Traits<D>::dtype == BTAS_F32, float, double>::type;
   LocalStats<A> st;
   const D inf = Traits<D>::eps(min_plus);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const S x = src[i];
-    D out;
-    if (x != x) {
-      st.nan++;
-      out = inf;
-    } else if (x == (S)-INFINITY) {
-      st.neg_inf++;
-      out = inf;
-    } else if (x == (S)INFINITY) {
-      out = inf;  // symbolic Infinity -> oriented (matrix.py:92-94)
-    } else {
-      const S v = x + (S)0;  // -0.0 -> +0.0 (matrix.py:92)
-      if constexpr (Traits<D>::dtype == BTAS_I32) {
-        if (v != floor(v) || fabs(v) >= (S)kI32Limit) {
-          st.out_of_range++;
-          out = 0;
-        } else {
-          out = (int32_t)v;
-        }
-        st.add_finite((A)v, (A)Traits<D>::int_limit);
-      } else {
-        out = (D)v;
-        if (isinf(out)) {
-          st.out_of_range++;  // finite double beyond the float range
-        } else {
-          st.add_finite((A)out, (A)Traits<D>::int_limit);
-        }
-      }
-    }
-    dst[i] = out;
+  // 4 independent elements per thread per trip: 4 loads in flight per thread
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i0 + 3 * stride < n; i0 += 4 * stride) {
+    S xs[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) xs[u] = src[i0 + u * stride];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dst[i0 + u * stride] = ingest_one<S, D, A>(xs[u], inf, st);
   }
+  for (int64_t i = i0; i < n; i += stride) dst[i] = ingest_one<S, D, A>(src[i], inf, st);
   commit(st, stats);
 }
 

@@ -127,15 +127,23 @@ __global__ void ext_rows_kernel(const T* __restrict__ B, int64_t ldb, int64_t K,
   const T* row = B + k * ldb;
   T mx = lowest<T>(), mn = highest<T>();
   bool any = false;
-#pragma unroll 4
-  for (int64_t j = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.y * blockDim.x) {
-    const T x = row[j];
+  auto take = [&](T x) {
     if (Traits<T>::finite(x)) {
       mx = x > mx ? x : mx;
       mn = x < mn ? x : mn;
       any = true;
     }
+  };
+  const int64_t stride = (int64_t)gridDim.y * blockDim.x;
+  int64_t j = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
+  for (; j + 3 * stride < N; j += 4 * stride) {  // 4 loads in flight per thread
+    T xs[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) xs[u] = row[j + u * stride];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) take(xs[u]);
   }
+  for (; j < N; j += stride) take(row[j]);
   double dmx = any ? (double)mx : -INFINITY, dmn = any ? (double)mn : INFINITY;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
