@@ -28,10 +28,10 @@ namespace btas {
 namespace {
 
 struct FwCtrl {
-  // snapshots of a pivot block left the s16 domain: [0]/[1] per block
-  // parity, [2] for the pair of blocks merged into one phase-3 pass
+  // snapshots of some pivot block of the current lookahead group left the
+  // s16 domain (reset by the group's first phase 1, OR-ed by every phase)
   int32_t s16_overflow[3];
-  int32_t pad[61];
+  int32_t pad[61];  // 256 bytes
 };
 
 // ------------------------------------------------------------------ rounds
@@ -100,7 +100,7 @@ struct FwArgs {
   int64_t Kp2;       // k-pair stride of the packed panels (capacity: two pivot blocks = b)
   int64_t Kp2w;      // word-pair stride of the s16 panels (b / 2)
   int koff;          // k offset of this pivot block inside the panels (0 or b)
-  int parity;        // which s16 flag this block reports to
+  int group_start;   // 1: first pivot block of a lookahead group (resets the s16 flag)
   int emit_s16;      // also emit the int16x2 operands
   int32_t* flags;
   FwCtrl* ctrl;
@@ -184,8 +184,7 @@ __global__ void __launch_bounds__(kFwThreads) fw_phase1_kernel(T* __restrict__ D
   T* cT = rs + b * b;
   const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
   if (threadIdx.x == 0) {
-    f.ctrl->s16_overflow[f.parity] = 0;
-    if (f.parity == 0) f.ctrl->s16_overflow[2] = 0;
+    if (f.group_start) f.ctrl->s16_overflow[0] = 0;
   }
   T v[R][R];
   load_block(D, f, f.k0, f.k0, ty, tx, v);
@@ -225,8 +224,7 @@ __global__ void __launch_bounds__(kFwThreads) fw_phase1_kernel(T* __restrict__ D
   bool out16 = emit_history(cT, f.k0, f.BMa, f, Scol, Scol16);
   out16 |= emit_history(rs, f.k0, f.BNb, f, Srow, Srow16);
   if (__syncthreads_or(out16) && threadIdx.x == 0) {
-    atomicOr(&f.ctrl->s16_overflow[f.parity], 1);
-    atomicOr(&f.ctrl->s16_overflow[2], 1);
+    atomicOr(&f.ctrl->s16_overflow[0], 1);
   }
   if (MODE == kChecked && __any_sync(0xffffffffu, sat) && (threadIdx.x & 31) == 0)
     atomicOr(&f.flags[BTAS_FLAG_SATURATED], 1);
@@ -293,8 +291,7 @@ __global__ void __launch_bounds__(kFwThreads) fw_phase2_kernel(T* __restrict__ D
   const bool out16 = row_panel ? emit_history(hist, c0, f.BNb, f, Srow, Srow16)
                                : emit_history(hist, r0, f.BMa, f, Scol, Scol16);
   if (__syncthreads_or(out16) && threadIdx.x == 0) {
-    atomicOr(&f.ctrl->s16_overflow[f.parity], 1);
-    atomicOr(&f.ctrl->s16_overflow[2], 1);
+    atomicOr(&f.ctrl->s16_overflow[0], 1);
   }
   if (MODE == kChecked && __any_sync(0xffffffffu, sat) && (threadIdx.x & 31) == 0)
     atomicOr(&f.flags[BTAS_FLAG_SATURATED], 1);
@@ -319,6 +316,8 @@ struct FwGeom {
   static constexpr int b = FwB<T>::b;
   static constexpr int BMa = sizeof(T) == 8 ? 64 : 128;
   static constexpr int BNb = 128;
+  // lookahead group size: 4-byte storage has b == every GEMM tile edge
+  static constexpr int look = sizeof(T) == 4 ? 8 : 1;
 };
 
 template <class T>
@@ -353,13 +352,13 @@ FwWs fw_ws(int64_t n) {
   w.csp = off;
   off += a256((size_t)G::b * G::b * sizeof(T));
   w.scol = off;
-  off += a256((size_t)rows * 2 * G::b * sizeof(T));  // two pivot blocks of k
+  off += a256((size_t)rows * G::look * G::b * sizeof(T));  // kLook pivot blocks of k
   w.srow = off;
-  off += a256((size_t)cols * 2 * G::b * sizeof(T));
+  off += a256((size_t)cols * G::look * G::b * sizeof(T));
   w.scol16 = off;
-  off += a256((size_t)rows * G::b * 4);
+  off += a256((size_t)rows * G::look * G::b / 2 * 4);
   w.srow16 = off;
-  off += a256((size_t)cols * G::b * 4);
+  off += a256((size_t)cols * G::look * G::b / 2 * 4);
   w.total = off;
   return w;
 }
@@ -375,6 +374,7 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
   const double limit = Traits<T>::dtype == BTAS_I32 ? (double)kI32Limit : Traits<T>::int_limit;
   (void)max_abs;
   constexpr bool CHECKED = MODE == kChecked;
+  constexpr int kLook = G::look;
 
   FwCtrl* ctrl = reinterpret_cast<FwCtrl*>(ws + W.ctrl);
   T* rsp = reinterpret_cast<T*>(ws + W.rsp);
@@ -401,8 +401,8 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
   f.limit = limit;
   f.BMa = G::BMa;
   f.BNb = G::BNb;
-  f.Kp2 = b;       // panels hold two pivot blocks: 2b k values = b k-pairs
-  f.Kp2w = b / 2;  // 2b k values = b words = b/2 word pairs
+  f.Kp2 = (int64_t)kLook * b / 2;  // panels hold kLook pivot blocks of k
+  f.Kp2w = (int64_t)kLook * b / 4;
   f.emit_s16 = emit_s16 ? 1 : 0;
   f.flags = flags;
   f.ctrl = ctrl;
@@ -427,7 +427,7 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
   g.Ap = scol;
   g.Bp = srow;
   g.Kp2 = b / 2;
-  g.Kp2s = b;
+  g.Kp2s = (int64_t)kLook * b / 2;
   g.M = n;
   g.N = n;
   g.mblocks = (int)(rows / G::BMa);
@@ -446,25 +446,21 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
   g16.Ap = scol16;
   g16.Bp = srow16;
   g16.Kp2 = b / 4;
-  g16.Kp2s = b / 2;
+  g16.Kp2s = (int64_t)kLook * b / 4;
   g16.mblocks = (int)(round_up(rows, 128) / 128);
   g16.nblocks = (int)(round_up(cols, 128) / 128);
   g16.gate_value = 0;
   g16.limit = limit;
   g16.integer_mode = 1;
 
-  // one phase-3 style update: 32-bit kernel gated on "s16 overflow", s16x2
-  // kernel gated on "no overflow" (flag word `fl`); half = first k half used,
-  // halves = 1 (K = b) or 2 (K = 2b, two pivot blocks merged)
-  auto phase3 = [&](GemmArgs a, GemmArgs a16, int fl, int half, int halves) -> int {
+  // one phase-3 style update over K = halves * b (pivot-block slots
+  // [0, halves) of the panels): 32-bit kernel gated on "s16 overflow",
+  // s16x2 kernel gated on "no overflow"
+  auto phase3 = [&](GemmArgs a, GemmArgs a16, int halves) -> int {
     a.Kp2 = (int64_t)halves * b / 2;
     a16.Kp2 = (int64_t)halves * b / 4;
-    a.Ap = static_cast<const T*>(a.Ap) + (size_t)half * (b / 2) * G::BMa * 2;
-    a.Bp = static_cast<const T*>(a.Bp) + (size_t)half * (b / 2) * G::BNb * 2;
-    a16.Ap = static_cast<const uint32_t*>(a16.Ap) + (size_t)half * (b / 4) * 128 * 2;
-    a16.Bp = static_cast<const uint32_t*>(a16.Bp) + (size_t)half * (b / 4) * 128 * 2;
-    a.gate = emit_s16 ? &ctrl->s16_overflow[fl] : nullptr;
-    a16.gate = &ctrl->s16_overflow[fl];
+    a.gate = emit_s16 ? &ctrl->s16_overflow[0] : nullptr;
+    a16.gate = &ctrl->s16_overflow[0];
     int rc;
     if constexpr (CHECKED) {
       rc = launch_gemm_epi<MixChecked<T, true>, true, kEpiAcc>(a, st);
@@ -479,10 +475,10 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
     if (emit_s16) rc = launch_gemm_epi<MixS16<true, T>, true, kEpiAcc>(a16, st);
     return rc;
   };
-  auto phases12 = [&](int kb) -> int {
+  auto phases12 = [&](int kb, int slot) -> int {
     f.k0 = (int64_t)kb * b;
-    f.parity = kb & 1;
-    f.koff = (kb & 1) * b;
+    f.koff = slot * b;
+    f.group_start = slot == 0;
     fw_phase1_kernel<T, MODE><<<1, kFwThreads, smem1, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
     if (nblk > 1)
       fw_phase2_kernel<T, MODE><<<dim3(nblk, 2), kFwThreads, smem2, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
@@ -490,58 +486,54 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
     return BTAS_OK;
   };
 
-  // Lookahead by one pivot block (4-byte storage; b == the GEMM tile edge):
-  // block kb's phase-3 update is applied right away only to the row and
-  // column panels of block kb+1 (which block kb+1's phases 1/2 read), and
-  // for every other tile it is merged with block kb+1's update into ONE
-  // K = 2b pass.  Candidates are formed from the same snapshots either way
-  // and min is order-free, so D is unchanged; the bulk pass does twice the
-  // add-min work per epilogue (tile load + store of D).
-  constexpr bool kLookahead = sizeof(T) == 4;
+  // Lookahead groups of kLook pivot blocks (4-byte storage, where b equals
+  // the GEMM tile edge).  Inside a group, block kb0+j's row and column
+  // panels first receive the pending updates of blocks kb0..kb0+j-1 (thin
+  // passes, K = j*b) — exactly what its phases 1/2 read — and every other
+  // tile receives all kLook updates at the end in ONE pass with K = kLook*b.
+  // Each candidate is formed from the same per-round snapshots as in the
+  // sequential program and min is order-free (re-applying a block's
+  // candidates to a tile that already has them changes nothing), so D is
+  // unchanged; the bulk pass does kLook times the add-min work per epilogue.
   int rc;
-  for (int kb = 0; kb < nblk; kb += kLookahead ? 2 : 1) {
-    if ((rc = phases12(kb))) return rc;
+  for (int kb0 = 0; kb0 < nblk; kb0 += kLook) {
+    const int m = std::min(kLook, nblk - kb0);
+    for (int j = 0; j < m; ++j) {
+      const int kb = kb0 + j;
+      const int64_t kk = (int64_t)kb * b, mk = std::min<int64_t>(b, n - kk);
+      if (j > 0) {
+        {  // pending updates -> row block kb
+          GemmArgs a = g, a16 = g16;
+          a.M = a16.M = mk;
+          a.mblocks = a16.mblocks = 1;
+          a.Ap = static_cast<const T*>(g.Ap) + (size_t)kb * g.Kp2s * G::BMa * 2;
+          a16.Ap = static_cast<const uint32_t*>(g16.Ap) + (size_t)kb * g16.Kp2s * 128 * 2;
+          a.C = a16.C = D + kk * ld;
+          a.Z = a16.Z = D + kk * ld;
+          if ((rc = phase3(a, a16, j))) return rc;
+        }
+        {  // pending updates -> column block kb (its rows in block kb just done)
+          GemmArgs a = g, a16 = g16;
+          a.N = a16.N = mk;
+          a.nblocks = a16.nblocks = 1;
+          a.Bp = static_cast<const T*>(g.Bp) + (size_t)kb * g.Kp2s * G::BNb * 2;
+          a16.Bp = static_cast<const uint32_t*>(g16.Bp) + (size_t)kb * g16.Kp2s * 128 * 2;
+          a.C = a16.C = D + kk;
+          a.Z = a16.Z = D + kk;
+          a.skip_row_lo = a16.skip_row_lo = kk;
+          a.skip_row_hi = a16.skip_row_hi = kk + b;
+          if ((rc = phase3(a, a16, j))) return rc;
+        }
+      }
+      if ((rc = phases12(kb, j))) return rc;
+    }
     if (nblk == 1) break;
-    const int64_t k0 = (int64_t)kb * b;
-    if (!kLookahead || kb + 1 == nblk) {
-      GemmArgs a = g, a16 = g16;
-      a.skip_row_lo = a16.skip_row_lo = a.skip_col_lo = a16.skip_col_lo = k0;
-      a.skip_row_hi = a16.skip_row_hi = a.skip_col_hi = a16.skip_col_hi = k0 + b;
-      if ((rc = phase3(a, a16, kb & 1, kb & 1, 1))) return rc;
-      continue;
-    }
-    const int64_t k1 = k0 + b, m1 = std::min<int64_t>(b, n - k1);
-    {  // (a) block kb -> row panel of kb+1 (all columns except block kb)
-      GemmArgs a = g, a16 = g16;
-      a.M = a16.M = m1;
-      a.mblocks = a16.mblocks = 1;
-      a.Ap = static_cast<const T*>(g.Ap) + (size_t)(kb + 1) * g.Kp2s * G::BMa * 2;
-      a16.Ap = static_cast<const uint32_t*>(g16.Ap) + (size_t)(kb + 1) * g16.Kp2s * 128 * 2;
-      a.C = a16.C = D + k1 * ld;
-      a.Z = a16.Z = D + k1 * ld;
-      a.skip_col_lo = a16.skip_col_lo = k0;
-      a.skip_col_hi = a16.skip_col_hi = k0 + b;
-      if ((rc = phase3(a, a16, 0, 0, 1))) return rc;
-    }
-    {  // (b) block kb -> column panel of kb+1 (all rows except blocks kb, kb+1)
-      GemmArgs a = g, a16 = g16;
-      a.N = a16.N = m1;
-      a.nblocks = a16.nblocks = 1;
-      a.Bp = static_cast<const T*>(g.Bp) + (size_t)(kb + 1) * g.Kp2s * G::BNb * 2;
-      a16.Bp = static_cast<const uint32_t*>(g16.Bp) + (size_t)(kb + 1) * g16.Kp2s * 128 * 2;
-      a.C = a16.C = D + k1;
-      a.Z = a16.Z = D + k1;
-      a.skip_row_lo = a16.skip_row_lo = k0;
-      a.skip_row_hi = a16.skip_row_hi = k1 + b;
-      if ((rc = phase3(a, a16, 0, 0, 1))) return rc;
-    }
-    if ((rc = phases12(kb + 1))) return rc;
-    {  // (c) blocks kb and kb+1 together on every tile outside row/col block kb+1
-      GemmArgs a = g, a16 = g16;
-      a.skip_row_lo = a16.skip_row_lo = a.skip_col_lo = a16.skip_col_lo = k1;
-      a.skip_row_hi = a16.skip_row_hi = a.skip_col_hi = a16.skip_col_hi = k1 + b;
-      if ((rc = phase3(a, a16, 2, 0, 2))) return rc;
-    }
+    // all kLook updates on every tile outside the last block's row/col panels
+    const int64_t kl = (int64_t)(kb0 + m - 1) * b;
+    GemmArgs a = g, a16 = g16;
+    a.skip_row_lo = a16.skip_row_lo = a.skip_col_lo = a16.skip_col_lo = kl;
+    a.skip_row_hi = a16.skip_row_hi = a.skip_col_hi = a16.skip_col_hi = kl + b;
+    if ((rc = phase3(a, a16, m))) return rc;
   }
   return BTAS_OK;
 }
