@@ -462,6 +462,9 @@ def apsp_arm(args, rank, world, dev):
     if args.workload == "apsp" and world > 1:
         # config C4: row-sharded squaring, NCCL all-gather per step
         from paper_1701_04733_b200.sharded import apsp_by_squaring_distributed as solver  # noqa: F811
+    elif args.workload == "fw" and world > 1:
+        # row-sharded blocked FW, NCCL broadcast of the pivot row panel per block
+        from paper_1701_04733_b200.sharded import floyd_warshall_distributed as solver  # noqa: F811
     for _ in range(max(1, min(args.warmup, 3))):
         rep = solver(adj)
     torch.cuda.synchronize()
@@ -483,7 +486,7 @@ def apsp_arm(args, rank, world, dev):
     pairs = float(n) ** 3 * (1 if args.workload == "fw" else mults)
     res = {"metric": f"APSP time n={n}", "value": round(ms / 1e3, 4), "unit": "s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False,
-           "scaling": "strong" if (args.workload == "apsp" and world > 1) else "weak", "vs_baseline": None,
+           "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
            "dtype": "i32" if dtype == torch.int32 else "f32",
            "data": "synthetic",
            "config": {"workload": f"{args.workload}_n{n}", "graph": "random_graph p=0.5 weights 1..100",

@@ -168,6 +168,30 @@ int btas_fw(int dtype, int integer_mode, void* D, int64_t ld, int64_t n, int mas
             double max_abs, double min_finite, int32_t* dev_flags,
             void* workspace, size_t workspace_bytes, btas_stream_t stream);
 
+/* Row-sharded Floyd-Warshall for P processes (one per GPU): the same
+ * per-round operands as btas_fw, one pivot block kb at a time.  Each rank
+ * holds rows [slab_r0, slab_r0 + slab_rows) of D (slab_r0 a multiple of 128)
+ * at D_slab.  Per pivot block the host runs, in order:
+ *   PIVOT   on the rank owning row block kb (phase 1 + row panel),
+ *   a broadcast of the owner's workspace bytes [bcast_offset, +bcast_bytes)
+ *           to every rank (NCCL over NVLink),
+ *   COLS    on every rank (column panels of its rows),
+ *   UPDATE  on every rank (phase-3 update of its rows);
+ * INIT once before the first block and DIAG once at the end.  `masked` and
+ * `min_finite` must be the same on every rank (all-reduced scan of D). */
+enum {
+  BTAS_FW_STAGE_INIT = 0,
+  BTAS_FW_STAGE_PIVOT = 1,
+  BTAS_FW_STAGE_COLS = 2,
+  BTAS_FW_STAGE_UPDATE = 3,
+  BTAS_FW_STAGE_DIAG = 4
+};
+size_t btas_fw_dist_workspace_bytes(int dtype, int64_t n, int64_t slab_rows, size_t* bcast_offset,
+                                    size_t* bcast_bytes);
+int btas_fw_dist_stage(int dtype, int integer_mode, int stage, void* D_slab, int64_t ld, int64_t n,
+                       int64_t slab_r0, int64_t slab_rows, int64_t kb, int masked, double min_finite,
+                       int32_t* dev_flags, void* workspace, size_t workspace_bytes, btas_stream_t stream);
+
 /* Diagonal test: sets BTAS_FLAG_DIAG_NEG if any d[i,i] < 0 (apsp.py:125,168). */
 int btas_diag_negative(int dtype, const void* d, int64_t ld, int64_t n, int32_t* dev_flags,
                        btas_stream_t stream);

@@ -101,6 +101,11 @@ struct FwArgs {
   int64_t Kp2w;      // word-pair stride of the s16 panels (b / 2)
   int koff;          // k offset of this pivot block inside the panels (0 or b)
   int group_start;   // 1: first pivot block of a lookahead group (resets the s16 flag)
+  // row slab held by this process: D points at global row slab_r0 and holds
+  // rows [slab_r0, slab_r1) (single GPU: the whole matrix)
+  int64_t slab_r0, slab_r1;
+  int panel_mode;    // phase 2 grid: 0 = y selects row (0) / column (1) panels, 1 = rows only, 2 = columns only
+  int col_blk0;      // first row block of the column panels (blockIdx.x offset)
   int emit_s16;      // also emit the int16x2 operands
   int32_t* flags;
   FwCtrl* ctrl;
@@ -122,7 +127,7 @@ BTAS_D void load_block(const T* __restrict__ D, const FwArgs& f, int64_t r0, int
 #pragma unroll
     for (int j = 0; j < R; ++j) {
       const int64_t col = c0 + tx * R + j;
-      v[i][j] = (row < f.n && col < f.n) ? D[row * f.ld + col] : inf;
+      v[i][j] = (row < f.slab_r1 && col < f.n) ? D[(row - f.slab_r0) * f.ld + col] : inf;
     }
   }
 }
@@ -137,7 +142,7 @@ BTAS_D void store_block(T* __restrict__ D, const FwArgs& f, int64_t r0, int64_t 
 #pragma unroll
     for (int j = 0; j < R; ++j) {
       const int64_t col = c0 + tx * R + j;
-      if (row < f.n && col < f.n) D[row * f.ld + col] = v[i][j];
+      if (row < f.slab_r1 && col < f.n) D[(row - f.slab_r0) * f.ld + col] = v[i][j];
     }
   }
 }
@@ -221,7 +226,7 @@ __global__ void __launch_bounds__(kFwThreads) fw_phase1_kernel(T* __restrict__ D
     colsnapT[e] = cT[e];
   }
   // pivot rows of Scol (A operand) and pivot columns of Srow (B operand)
-  bool out16 = emit_history(cT, f.k0, f.BMa, f, Scol, Scol16);
+  bool out16 = emit_history(cT, f.k0 - f.slab_r0, f.BMa, f, Scol, Scol16);  // Scol rows are slab-local
   out16 |= emit_history(rs, f.k0, f.BNb, f, Srow, Srow16);
   if (__syncthreads_or(out16) && threadIdx.x == 0) {
     atomicOr(&f.ctrl->s16_overflow[0], 1);
@@ -240,9 +245,9 @@ __global__ void __launch_bounds__(kFwThreads) fw_phase2_kernel(T* __restrict__ D
                                                                T* __restrict__ Srow, uint32_t* __restrict__ Scol16,
                                                                uint32_t* __restrict__ Srow16, FwArgs f) {
   constexpr int b = FwB<T>::b, R = FwB<T>::R;
-  const int blk = blockIdx.x;
+  const bool row_panel = f.panel_mode == 0 ? blockIdx.y == 0 : f.panel_mode == 1;
+  const int blk = row_panel ? (int)blockIdx.x : f.col_blk0 + (int)blockIdx.x;
   if (blk == (int)(f.k0 / b)) return;
-  const bool row_panel = blockIdx.y == 0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* fixed = reinterpret_cast<T*>(smem_raw);  // row panel: colsnapT[k][a]; col panel: rowsnapP[k][c]
   T* hist = fixed + b * b;                      // row panel: rs[k][c];      col panel: cT[k][a]
@@ -289,7 +294,7 @@ __global__ void __launch_bounds__(kFwThreads) fw_phase2_kernel(T* __restrict__ D
   store_block(D, f, r0, c0, ty, tx, v);
   __syncthreads();
   const bool out16 = row_panel ? emit_history(hist, c0, f.BNb, f, Srow, Srow16)
-                               : emit_history(hist, r0, f.BMa, f, Scol, Scol16);
+                               : emit_history(hist, r0 - f.slab_r0, f.BMa, f, Scol, Scol16);
   if (__syncthreads_or(out16) && threadIdx.x == 0) {
     atomicOr(&f.ctrl->s16_overflow[0], 1);
   }
@@ -396,6 +401,8 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
   FwArgs f{};
   f.n = n;
   f.ld = ld;
+  f.slab_r0 = 0;
+  f.slab_r1 = n;
   f.nblk = nblk;
   f.int_mode = int_mode ? 1 : 0;
   f.limit = limit;
@@ -538,6 +545,177 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
   return BTAS_OK;
 }
 
+// ------------------------------------------------------------------ distributed
+// Row-slab Floyd-Warshall for P processes (one per GPU), one pivot block at a
+// time (no lookahead): the owner of pivot block kb runs phase 1 and the row
+// panel, the "broadcast region" of its workspace (pivot snapshots, packed
+// row-panel snapshots in both forms, the s16 flag) is broadcast by the host
+// (NCCL), then every rank runs the column panels and the phase-3 update of its
+// own rows.  Same per-round candidates as the single-GPU program, so D is
+// byte-identical for any P.
+struct FwDistWs {
+  size_t ctrl, rsp, csp, srow, srow16, bcast_end, scol, scol16, total;
+};
+
+template <class T>
+FwDistWs fw_dist_ws(int64_t n, int64_t slab_rows) {
+  using G = FwGeom<T>;
+  const int64_t rows = std::max<int64_t>(round_up(std::max<int64_t>(slab_rows, 1), 128), G::b);
+  const int64_t cols = fw_cols<T>(n);
+  FwDistWs w;
+  size_t off = 0;
+  w.ctrl = off;
+  off += a256(sizeof(FwCtrl));
+  w.rsp = off;
+  off += a256((size_t)G::b * G::b * sizeof(T));
+  w.csp = off;
+  off += a256((size_t)G::b * G::b * sizeof(T));
+  w.srow = off;
+  off += a256((size_t)cols * G::b * sizeof(T));
+  w.srow16 = off;
+  off += a256((size_t)cols * (G::b / 2) * 4);
+  w.bcast_end = off;
+  w.scol = off;
+  off += a256((size_t)rows * G::b * sizeof(T));
+  w.scol16 = off;
+  off += a256((size_t)rows * (G::b / 2) * 4);
+  w.total = off;
+  return w;
+}
+
+template <class T, int MODE>
+int fw_dist_stage_typed(int integer_mode, int stage, T* D, int64_t ld, int64_t n, int64_t slab_r0, int64_t slab_rows,
+                        int64_t kb, int32_t* flags, unsigned char* ws, cudaStream_t st) {
+  using G = FwGeom<T>;
+  constexpr int b = G::b;
+  constexpr bool CHECKED = MODE == kChecked;
+  const FwDistWs W = fw_dist_ws<T>(n, slab_rows);
+  const int nblk = (int)ceil_div(n, b);
+  const bool int_mode = Traits<T>::dtype == BTAS_I32 || integer_mode;
+  const double limit = Traits<T>::dtype == BTAS_I32 ? (double)kI32Limit : Traits<T>::int_limit;
+  const bool emit_s16 = int_mode && !CHECKED;
+  FwCtrl* ctrl = reinterpret_cast<FwCtrl*>(ws + W.ctrl);
+  T* rsp = reinterpret_cast<T*>(ws + W.rsp);
+  T* csp = reinterpret_cast<T*>(ws + W.csp);
+  T* srow = reinterpret_cast<T*>(ws + W.srow);
+  uint32_t* srow16 = reinterpret_cast<uint32_t*>(ws + W.srow16);
+  T* scol = reinterpret_cast<T*>(ws + W.scol);
+  uint32_t* scol16 = reinterpret_cast<uint32_t*>(ws + W.scol16);
+  const int64_t rows_pad = (int64_t)((W.scol16 - W.scol) / sizeof(T)) / b;
+
+  FwArgs f{};
+  f.n = n;
+  f.ld = ld;
+  f.slab_r0 = slab_r0;
+  f.slab_r1 = slab_r0 + slab_rows;
+  f.k0 = kb * b;
+  f.nblk = nblk;
+  f.int_mode = int_mode ? 1 : 0;
+  f.limit = limit;
+  f.BMa = G::BMa;
+  f.BNb = G::BNb;
+  f.Kp2 = b / 2;
+  f.Kp2w = b / 4;
+  f.koff = 0;
+  f.group_start = 1;
+  f.emit_s16 = emit_s16 ? 1 : 0;
+  f.flags = flags;
+  f.ctrl = ctrl;
+  const size_t smem = 2 * (size_t)b * b * sizeof(T);
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(fw_phase1_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(fw_phase2_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess) {
+      (void)cudaGetLastError();
+      return BTAS_ERR_CUDA;
+    }
+    configured = true;
+  }
+  switch (stage) {
+    case BTAS_FW_STAGE_INIT: {
+      // packed panels: padding rows/cols hold Infinity
+      fill_t_kernel<T><<<1024, 256, 0, st>>>(srow, (int64_t)((W.srow16 - W.srow) / sizeof(T)), Traits<T>::eps(true));
+      fill_t_kernel<T><<<1024, 256, 0, st>>>(scol, (int64_t)((W.scol16 - W.scol) / sizeof(T)), Traits<T>::eps(true));
+      const uint32_t inf16 = (uint32_t)kS16Inf | ((uint32_t)kS16Inf << 16);
+      fill_u32_kernel<<<1024, 256, 0, st>>>(srow16, (int64_t)((W.bcast_end - W.srow16) / 4), inf16);
+      fill_u32_kernel<<<1024, 256, 0, st>>>(scol16, (int64_t)((W.total - W.scol16) / 4), inf16);
+      break;
+    }
+    case BTAS_FW_STAGE_PIVOT: {
+      if (f.k0 < slab_r0 || f.k0 >= slab_r0 + slab_rows) return BTAS_ERR_INVALID;  // not the owner
+      fw_phase1_kernel<T, MODE><<<1, kFwThreads, smem, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
+      if (nblk > 1) {
+        f.panel_mode = 1;
+        fw_phase2_kernel<T, MODE><<<dim3(nblk, 1), kFwThreads, smem, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
+      }
+      break;
+    }
+    case BTAS_FW_STAGE_COLS: {
+      if (slab_rows == 0 || nblk == 1) break;
+      f.panel_mode = 2;
+      f.col_blk0 = (int)(slab_r0 / b);
+      const int nsb = (int)ceil_div(slab_rows, b);
+      fw_phase2_kernel<T, MODE><<<dim3(nsb, 1), kFwThreads, smem, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
+      break;
+    }
+    case BTAS_FW_STAGE_UPDATE: {
+      if (slab_rows == 0 || nblk == 1) break;
+      GemmArgs g{};
+      g.Ap = scol;
+      g.Bp = srow;
+      g.Kp2 = b / 2;
+      g.M = slab_rows;
+      g.N = n;
+      g.mblocks = (int)(rows_pad / G::BMa);
+      g.nblocks = (int)(fw_cols<T>(n) / G::BNb);
+      g.Z = D;
+      g.ldz = ld;
+      g.C = D;
+      g.ldc = ld;
+      g.flags = flags;
+      g.integer_mode = int_mode ? 1 : 0;
+      g.limit = int_mode ? limit : INFINITY;
+      g.no_diag = 1;
+      g.skip_row_lo = f.k0 - slab_r0;
+      g.skip_row_hi = f.k0 - slab_r0 + b;
+      g.skip_col_lo = f.k0;
+      g.skip_col_hi = f.k0 + b;
+      g.gate = emit_s16 ? &ctrl->s16_overflow[0] : nullptr;
+      g.gate_value = 1;
+      GemmArgs g16 = g;
+      g16.Ap = scol16;
+      g16.Bp = srow16;
+      g16.Kp2 = b / 4;
+      g16.mblocks = (int)(round_up(rows_pad, 128) / 128);
+      g16.nblocks = (int)(round_up(fw_cols<T>(n), 128) / 128);
+      g16.gate = &ctrl->s16_overflow[0];
+      g16.gate_value = 0;
+      g16.limit = limit;
+      g16.integer_mode = 1;
+      int rc;
+      if constexpr (CHECKED) rc = launch_gemm_epi<MixChecked<T, true>, true, kEpiAcc>(g, st);
+      else if constexpr (Traits<T>::dtype == BTAS_F64) rc = launch_gemm_epi<MixF64<true>, true, kEpiAcc>(g, st);
+      else if constexpr (Traits<T>::dtype == BTAS_I32) rc = launch_gemm_epi<MixI32<true>, true, kEpiAcc>(g, st);
+      else rc = launch_gemm_epi<MixF32<true>, true, kEpiAcc>(g, st);
+      if (rc) return rc;
+      if (emit_s16) {
+        rc = launch_gemm_epi<MixS16<true, T>, true, kEpiAcc>(g16, st);
+        if (rc) return rc;
+      }
+      break;
+    }
+    case BTAS_FW_STAGE_DIAG:
+      if (slab_rows > 0) return btas_diag_negative(Traits<T>::dtype, D + slab_r0, ld, slab_rows, flags, st);
+      break;
+    default:
+      return BTAS_ERR_INVALID;
+  }
+  BTAS_CUDA_CHECK_LAUNCH();
+  return BTAS_OK;
+}
+
 }  // namespace
 }  // namespace btas
 
@@ -586,4 +764,64 @@ extern "C" int btas_fw(int dtype, int integer_mode, void* D, int64_t ld, int64_t
 #undef BTAS_FW_CALL
   if (rc) return rc;
   return btas_diag_negative(dtype, D, ld, n, dev_flags, stream);
+}
+
+extern "C" size_t btas_fw_dist_workspace_bytes(int dtype, int64_t n, int64_t slab_rows, size_t* bcast_offset,
+                                               size_t* bcast_bytes) {
+  if (n < 1 || slab_rows < 0) return 0;
+  size_t total = 0, off = 0, end = 0;
+  switch (dtype) {
+    case BTAS_F32: {
+      const FwDistWs w = fw_dist_ws<float>(n, slab_rows);
+      total = w.total, off = w.ctrl, end = w.bcast_end;
+      break;
+    }
+    case BTAS_I32: {
+      const FwDistWs w = fw_dist_ws<int32_t>(n, slab_rows);
+      total = w.total, off = w.ctrl, end = w.bcast_end;
+      break;
+    }
+    case BTAS_F64: {
+      const FwDistWs w = fw_dist_ws<double>(n, slab_rows);
+      total = w.total, off = w.ctrl, end = w.bcast_end;
+      break;
+    }
+    default:
+      return 0;
+  }
+  if (bcast_offset) *bcast_offset = off;
+  if (bcast_bytes) *bcast_bytes = end - off;
+  return total;
+}
+
+extern "C" int btas_fw_dist_stage(int dtype, int integer_mode, int stage, void* D_slab, int64_t ld, int64_t n,
+                                  int64_t slab_r0, int64_t slab_rows, int64_t kb, int masked, double min_finite,
+                                  int32_t* dev_flags, void* workspace, size_t workspace_bytes, btas_stream_t stream) {
+  if (!dev_flags || !workspace || n < 1 || ld < n || slab_r0 < 0 || slab_rows < 0 || slab_r0 + slab_rows > n)
+    return BTAS_ERR_INVALID;
+  if (slab_rows > 0 && !D_slab) return BTAS_ERR_INVALID;
+  const int64_t b = dtype == BTAS_F64 ? 64 : 128;
+  if ((slab_rows > 0 && slab_r0 % 128 != 0) || kb < 0 || kb * b >= n) return BTAS_ERR_INVALID;
+  if (workspace_bytes < btas_fw_dist_workspace_bytes(dtype, n, slab_rows, nullptr, nullptr)) return BTAS_ERR_WORKSPACE;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  unsigned char* ws = static_cast<unsigned char*>(workspace);
+#define BTAS_FWD_CALL(T)                                                                                          \
+  (masked ? fw_dist_stage_typed<T, kChecked>(integer_mode, stage, (T*)D_slab, ld, n, slab_r0, slab_rows, kb,      \
+                                             dev_flags, ws, st)                                                   \
+   : (dtype == BTAS_I32 && min_finite < 0.0)                                                                      \
+       ? fw_dist_stage_typed<T, kClamp>(integer_mode, stage, (T*)D_slab, ld, n, slab_r0, slab_rows, kb, dev_flags, \
+                                        ws, st)                                                                   \
+       : fw_dist_stage_typed<T, kFast>(integer_mode, stage, (T*)D_slab, ld, n, slab_r0, slab_rows, kb, dev_flags,  \
+                                       ws, st))
+  switch (dtype) {
+    case BTAS_F32:
+      return BTAS_FWD_CALL(float);
+    case BTAS_I32:
+      return BTAS_FWD_CALL(int32_t);
+    case BTAS_F64:
+      return BTAS_FWD_CALL(double);
+    default:
+      return BTAS_ERR_INVALID;
+  }
+#undef BTAS_FWD_CALL
 }

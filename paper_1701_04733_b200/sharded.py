@@ -158,3 +158,164 @@ def apsp_by_squaring_sharded(base: torch.Tensor, group=None, gemm_rows: "Callabl
         sat |= bool(f[2])
         negative = bool(f[0]) or bool(f[1])
     return ShardedResult(res_d, negative, mults, sat)
+
+
+# ---------------------------------------------------------------------------
+# row-sharded Floyd-Warshall (pivot-panel broadcast)
+# ---------------------------------------------------------------------------
+FW_STAGE_INIT, FW_STAGE_PIVOT, FW_STAGE_COLS, FW_STAGE_UPDATE, FW_STAGE_DIAG = 0, 1, 2, 3, 4
+
+
+class _FwRank:
+    """One rank's slab, workspace and flag words for btas_fw_dist_stage."""
+
+    def __init__(self, rank, r0, rows, slab, code, n, dev):
+        import ctypes
+
+        self.rank, self.r0, self.rows, self.slab = rank, r0, rows, slab
+        off, nb = ctypes.c_size_t(), ctypes.c_size_t()
+        total = _lib.load().btas_fw_dist_workspace_bytes(code, n, rows, ctypes.byref(off), ctypes.byref(nb))
+        self.ws = torch.empty(total, dtype=torch.uint8, device=dev)
+        self.region = self.ws[off.value : off.value + nb.value]
+        self.flags = torch.zeros(_lib.NUM_FLAGS, dtype=torch.int32, device=dev)
+
+
+def _fw_rows_run(ranks, code, integer, n, ld, masked, min_fin, b, chunk, bcast):
+    """The stage sequence of btas_fw_dist_stage (include/btas_cuda.h) over
+    the given local ranks; ``bcast(owner, ranks)`` moves the owner's
+    broadcast region to every rank."""
+    from .matrix import _ptr, _stream
+
+    def stage(rk, s, kb=0):
+        ptr = _ptr(rk.slab) if rk.rows > 0 else None
+        _lib.call("btas_fw_dist_stage", code, 1 if integer else 0, s, ptr, ld, n, rk.r0, rk.rows, kb,
+                  1 if masked else 0, min_fin, _ptr(rk.flags), _ptr(rk.ws), rk.ws.numel(), _stream(rk.ws.device))
+
+    for rk in ranks:
+        stage(rk, FW_STAGE_INIT)
+    nblk = -(-n // b)
+    for kb in range(nblk):
+        owner = (kb * b) // chunk
+        for rk in ranks:
+            if rk.rank == owner:
+                stage(rk, FW_STAGE_PIVOT, kb)
+        bcast(owner, ranks)
+        for rk in ranks:
+            stage(rk, FW_STAGE_COLS, kb)
+        for rk in ranks:
+            stage(rk, FW_STAGE_UPDATE, kb)
+    for rk in ranks:
+        stage(rk, FW_STAGE_DIAG)
+
+
+def _fw_setup(adj):
+    from .apsp import _closure_base, _fw_limit, _require_square_minplus
+    from .matrix import _dtype_code
+
+    n = _require_square_minplus(adj)
+    base = _closure_base(adj)
+    code = _dtype_code(base.dtype)
+    b = 64 if base.dtype == torch.float64 else 128
+    return n, base, code, b, _fw_limit(adj)
+
+
+def _slab_stats(slab, code):
+    """(max |finite|, min finite) of a slab as float64 device scalars (+inf/−inf if empty)."""
+    from .matrix import _new_stats, _ptr, _read_stats, _stream
+
+    dev = slab.device
+    if slab.numel() == 0:
+        return torch.tensor([0.0, float("inf")], dtype=torch.float64, device=dev)
+    st = _new_stats(dev)
+    _lib.call("btas_scan", code, _ptr(slab), slab.numel(), _ptr(st), _stream(dev))
+    s = _read_stats(st)
+    if s.finite_count == 0:
+        return torch.tensor([0.0, float("inf")], dtype=torch.float64, device=dev)
+    return torch.tensor([_lib.key_to_float(s.max_abs_key), _lib.key_to_float(s.min_key)], dtype=torch.float64,
+                        device=dev)
+
+
+def _fw_report(adj, d, negative):
+    from .apsp import Algorithm, ApspReport, DistanceMatrix
+    from .matrix import TropicalMatrix
+
+    n = adj.n_rows
+    m = TropicalMatrix._wrap(adj.kind, d, adj.integer)
+    return ApspReport(distances=DistanceMatrix(n, m), algorithm=Algorithm.FLOYD_WARSHALL,
+                      negative_cycle=negative, multiplications_performed=0)
+
+
+def floyd_warshall_distributed(adj, group=None):
+    """``floyd_warshall`` (reference apsp.py:93-133) with D row-sharded over
+    the ranks of ``group`` (one process per GPU, NCCL): per pivot block the
+    owning rank computes the pivot tile and row panel, broadcasts the packed
+    row-panel snapshots (b x n) over NVLink, and every rank updates its own
+    rows.  Every rank passes the same adjacency and receives the full result;
+    distances and the negative-cycle flag are byte-identical to the
+    single-GPU ``floyd_warshall`` for any number of ranks."""
+    from .semiring import _note_saturation
+
+    n, base, code, b, limit = _fw_setup(adj)
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    chunk, spans = partition(n, world)
+    r0, r1 = spans[rank]
+    d = base.data
+    ld = d.stride(0)
+    st = _slab_stats(d[r0:r1], code)
+    mx = st[:1].clone()
+    mn = st[1:].clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=group)
+    dist.all_reduce(mn, op=dist.ReduceOp.MIN, group=group)
+    max_abs, min_fin = float(mx.item()), float(mn.item())
+    masked = not (2.0 * (n + 1) * max_abs < limit)
+    rk = _FwRank(rank, r0, r1 - r0, d[r0:r1], code, n, d.device)
+
+    def bcast(owner, ranks):
+        dist.broadcast(ranks[0].region, src=dist.get_global_rank(group, owner) if group is not None else owner,
+                       group=group)
+
+    _fw_rows_run([rk], code, base.integer, n, ld, masked, min_fin, b, chunk, bcast)
+    flags = rk.flags.clone()
+    dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=group)
+    # gather the row slabs into the full distance matrix on every rank
+    full = torch.empty((world * chunk, n), dtype=d.dtype, device=d.device)
+    mine = full[rank * chunk : (rank + 1) * chunk]
+    if r1 > r0:
+        mine[: r1 - r0].copy_(d[r0:r1])
+    dist.all_gather_into_tensor(full, mine, group=group)
+    f = flags.cpu().tolist()
+    if f[_lib.FLAG_SATURATED]:
+        _note_saturation()
+    return _fw_report(adj, full[:n].contiguous() if world * chunk != n else full, bool(f[_lib.FLAG_DIAG_NEG]))
+
+
+def floyd_warshall_emulated(adj, world: int):
+    """The row-sharded program of ``floyd_warshall_distributed`` with
+    ``world`` virtual ranks executed in sequence on ONE GPU (slabs are row
+    ranges of one matrix, the broadcast is a device copy).  Exercises the
+    exact per-rank stage sequence and slab indexing of P > 1 where only one
+    GPU is available; the result must equal the single-GPU solve."""
+    from .semiring import _note_saturation
+
+    n, base, code, b, limit = _fw_setup(adj)
+    chunk, spans = partition(n, world)
+    d = base.data
+    ld = d.stride(0)
+    st = [_slab_stats(d[r0:r1], code) for r0, r1 in spans]
+    max_abs = max(float(s[0]) for s in st)
+    min_fin = min(float(s[1]) for s in st)
+    masked = not (2.0 * (n + 1) * max_abs < limit)
+    ranks = [_FwRank(r, r0, r1 - r0, d[r0:r1], code, n, d.device) for r, (r0, r1) in enumerate(spans)]
+
+    def bcast(owner, rks):
+        src = rks[owner].region
+        for rk in rks:
+            if rk.rank != owner:
+                rk.region.copy_(src)
+
+    _fw_rows_run(ranks, code, base.integer, n, ld, masked, min_fin, b, chunk, bcast)
+    f = torch.stack([rk.flags for rk in ranks]).amax(dim=0).cpu().tolist()
+    if f[_lib.FLAG_SATURATED]:
+        _note_saturation()
+    return _fw_report(adj, d, bool(f[_lib.FLAG_DIAG_NEG]))
