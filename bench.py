@@ -290,12 +290,22 @@ def main():
         "clocks": clk,
     }
 
+    if traffic is not None:
+        roofline["traffic_note"] = ("dram bytes per launch (ncu --set full); above the compulsory 2-3 GB because "
+                                    "L2 serves ~90 % of the 128 GB of tile loads — HBM runs at ~2 % of peak")
+
     # ------------------------------------------------------------- e2e (public API, host buffers)
     if not args.no_e2e:
-        result["e2e"] = e2e_gemm(n, dtype, xs, ys, dev, steps=max(3, min(args.steps, 6)))
+        e2e = e2e_gemm(n, dtype, xs, ys, dev, steps=max(3, min(args.steps, 6)))
+        if world > 1:  # whole job: every rank's steps over the slowest rank's time
+            t = torch.tensor([e2e["ms_per_step"]], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e["ms_per_step"] = round(float(t.item()), 2)
+            e2e["value"] = round(float(n) ** 3 * world / (e2e["ms_per_step"] * 1e-3) / 1e9, 1)
+        result["e2e"] = e2e
 
-    # ------------------------------------------------------------- other kernel paths
-    if not args.no_variants and args.workload == "gemm":
+    # ------------------------------------------------------------- other kernel paths (N = 1 only)
+    if not args.no_variants and args.workload == "gemm" and world == 1:
         result["variants"] = variants(n, dev, rank)
 
     # ------------------------------------------------------------- CPU baseline (rank 0, N = 1)
