@@ -470,7 +470,8 @@ def apsp_arm(args, rank, world, dev):
     adj = random_graph_matrix(n, 0.5, (1, 100), instance_seed(1, n), dtype=dtype, device=dev)
     solver = bt.floyd_warshall if args.workload == "fw" else bt.apsp_by_squaring
     if args.workload == "apsp" and world > 1:
-        # config C4: row-sharded squaring, NCCL all-gather per step
+        # config C4: row-sharded squaring; the all-gather is fused into the
+        # GEMM epilogue (peer stores into symmetric memory), NCCL fallback
         from paper_1701_04733_b200.sharded import apsp_by_squaring_distributed as solver  # noqa: F811
     elif args.workload == "fw" and world > 1:
         # row-sharded blocked FW, NCCL broadcast of the pivot row panel per block
@@ -502,6 +503,8 @@ def apsp_arm(args, rank, world, dev):
            "config": {"workload": f"{args.workload}_n{n}", "graph": "random_graph p=0.5 weights 1..100",
                       "multiplications": mults, "negative_cycle": rep.negative_cycle,
                       "gpairs_per_s": round(pairs / (ms * 1e-3) / 1e9, 1)}}
+    if args.workload == "apsp" and world > 1:
+        res["config"]["exchange"] = os.environ.get("BTAS_EXCHANGE", "auto")
     if rank == 0:
         print(json.dumps(res), flush=True)
     return 0

@@ -142,6 +142,20 @@ int btas_gemm(int dtype, int kind, int integer_mode,
               int32_t* dev_flags, void* workspace, size_t workspace_bytes,
               btas_stream_t stream);
 
+/* btas_gemm fused with an all-gather over peer memory: every element of C is
+ * also stored at the same offset into peer_C[0..n_peers) (n_peers <= 7) —
+ * the other ranks' buffers mapped into this process over NVLink (CUDA IPC /
+ * symmetric memory) — from the GEMM epilogue, so the exchange of row-sharded
+ * results overlaps the add-min work tile by tile (no separate collective).
+ * Peer stores are made visible system-wide before the kernel completes.
+ * Used by the row-sharded squaring step (apsp.py:159). */
+int btas_gemm_peers(int dtype, int kind, int integer_mode,
+                    const void* A, int64_t lda, const void* B, int64_t ldb,
+                    void* C, int64_t ldc, int64_t M, int64_t N, int64_t K,
+                    const void* Cprev, int64_t ldcp, void* const* peer_C, int n_peers,
+                    int32_t* dev_flags, void* workspace, size_t workspace_bytes,
+                    btas_stream_t stream);
+
 /* Measurement hooks (bench.py): when enabled, every btas_gemm brackets its
  * GEMM kernel launches (not the screen/packing) with CUDA events recorded on
  * the caller's stream; btas_gemm_timing_read synchronises on them and returns

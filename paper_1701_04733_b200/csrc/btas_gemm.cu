@@ -89,10 +89,13 @@ extern "C" size_t btas_gemm_workspace_bytes(int dtype, int64_t M, int64_t N, int
   return gemm_ws_total(dtype, M, N, K);
 }
 
-extern "C" int btas_gemm(int dtype, int kind, int integer_mode, const void* A, int64_t lda, const void* B,
-                         int64_t ldb, const void* Z, int64_t ldz, void* C, int64_t ldc, int64_t M, int64_t N,
-                         int64_t K, const void* Cprev, int64_t ldcp, int32_t* dev_flags, void* workspace,
-                         size_t workspace_bytes, btas_stream_t stream) {
+static int gemm_entry(int dtype, int kind, int integer_mode, const void* A, int64_t lda, const void* B, int64_t ldb,
+                      const void* Z, int64_t ldz, void* C, int64_t ldc, int64_t M, int64_t N, int64_t K,
+                      const void* Cprev, int64_t ldcp, int32_t* dev_flags, void* workspace, size_t workspace_bytes,
+                      void* const* peers, int n_peers, btas_stream_t stream) {
+  if (n_peers < 0 || n_peers > kMaxPeers || (n_peers > 0 && !peers)) return BTAS_ERR_INVALID;
+  for (int q = 0; q < n_peers; ++q)
+    if (!peers[q]) return BTAS_ERR_INVALID;
   if (!A || !B || !C || !dev_flags || !workspace) return BTAS_ERR_INVALID;
   if (M < 1 || N < 1 || K < 1 || lda < K || ldb < N || ldc < N) return BTAS_ERR_INVALID;
   if (Z && ldz < N) return BTAS_ERR_INVALID;
@@ -107,12 +110,28 @@ extern "C" int btas_gemm(int dtype, int kind, int integer_mode, const void* A, i
   switch (dtype) {
     case BTAS_F32:
       return gemm_f32(mn, integer_mode, (const float*)A, lda, (const float*)B, ldb, (const float*)Z, ldz, (float*)C,
-                      ldc, M, N, K, (const float*)Cprev, ldcp, dev_flags, ws, st);
+                      ldc, M, N, K, (const float*)Cprev, ldcp, dev_flags, ws, peers, n_peers, st);
     case BTAS_I32:
       return gemm_i32(mn, integer_mode, (const int32_t*)A, lda, (const int32_t*)B, ldb, (const int32_t*)Z, ldz,
-                      (int32_t*)C, ldc, M, N, K, (const int32_t*)Cprev, ldcp, dev_flags, ws, st);
+                      (int32_t*)C, ldc, M, N, K, (const int32_t*)Cprev, ldcp, dev_flags, ws, peers, n_peers, st);
     default:
       return gemm_f64(mn, integer_mode, (const double*)A, lda, (const double*)B, ldb, (const double*)Z, ldz,
-                      (double*)C, ldc, M, N, K, (const double*)Cprev, ldcp, dev_flags, ws, st);
+                      (double*)C, ldc, M, N, K, (const double*)Cprev, ldcp, dev_flags, ws, peers, n_peers, st);
   }
+}
+
+extern "C" int btas_gemm(int dtype, int kind, int integer_mode, const void* A, int64_t lda, const void* B,
+                         int64_t ldb, const void* Z, int64_t ldz, void* C, int64_t ldc, int64_t M, int64_t N,
+                         int64_t K, const void* Cprev, int64_t ldcp, int32_t* dev_flags, void* workspace,
+                         size_t workspace_bytes, btas_stream_t stream) {
+  return gemm_entry(dtype, kind, integer_mode, A, lda, B, ldb, Z, ldz, C, ldc, M, N, K, Cprev, ldcp, dev_flags,
+                    workspace, workspace_bytes, nullptr, 0, stream);
+}
+
+extern "C" int btas_gemm_peers(int dtype, int kind, int integer_mode, const void* A, int64_t lda, const void* B,
+                               int64_t ldb, void* C, int64_t ldc, int64_t M, int64_t N, int64_t K, const void* Cprev,
+                               int64_t ldcp, void* const* peer_C, int n_peers, int32_t* dev_flags, void* workspace,
+                               size_t workspace_bytes, btas_stream_t stream) {
+  return gemm_entry(dtype, kind, integer_mode, A, lda, B, ldb, nullptr, 0, C, ldc, M, N, K, Cprev, ldcp, dev_flags,
+                    workspace, workspace_bytes, peer_C, n_peers, stream);
 }

@@ -58,6 +58,12 @@ struct GemmArgs {
   int64_t skip_row_lo, skip_row_hi, skip_col_lo, skip_col_hi;
   int64_t Kp2s;          // k-pair stride between blocks of the packed buffers (0: = Kp2)
   int no_diag;           // 1: skip the diag<0 test (C is a window, not the whole matrix)
+  // fused all-gather: every output element is also stored, at the same
+  // offset, into up to kMaxPeers other buffers — the other ranks' copies
+  // mapped into this process (NVLink peer memory), so the exchange of
+  // row-sharded results overlaps the add-min work tile by tile
+  void* peer_C[7];
+  int n_peers;
   int integer_mode;
   double limit;          // saturation limit (integer limit, or +inf for float mode)
 };
@@ -304,7 +310,8 @@ struct GemmShape {
 // bit 1 = fixpoint reference Cprev present.  Separate instantiations keep the
 // plain product's epilogue minimal (measured: a generic epilogue costs the
 // n = 16384 GEMM ~1 %, profiles/r01_experiments.md).
-enum { kEpiPlain = 0, kEpiAcc = 1, kEpiCmp = 2, kEpiBoth = 3 };
+enum { kEpiPlain = 0, kEpiAcc = 1, kEpiCmp = 2, kEpiBoth = 3, kEpiPeers = 4 };
+constexpr int kMaxPeers = 7;
 
 template <class P, bool MIN, int EPI>
 __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __grid_constant__ GemmArgs g) {
@@ -465,6 +472,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
             if (Cp != nullptr) changed |= bits_differ(v[0], xi[i][r][j][0]) | bits_differ(v[1], xi[i][r][j][1]);
             if (diag_tile) diag_neg |= (row == col0 && v[0] < (Out)0) | (row == col0 + 1 && v[1] < (Out)0);
             st2(C + row * g.ldc + col0, v);
+            if constexpr ((EPI & kEpiPeers) != 0) {
+#pragma unroll 1
+              for (int q = 0; q < g.n_peers; ++q) st2(static_cast<Out*>(g.peer_C[q]) + row * g.ldc + col0, v);
+            }
           }
         }
       continue;
@@ -521,9 +532,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
             if (col0 < g.N) C[row * g.ldc + col0] = v[0];
             if (col0 + 1 < g.N) C[row * g.ldc + col0 + 1] = v[1];
           }
+          if constexpr ((EPI & kEpiPeers) != 0) {
+#pragma unroll 1
+            for (int q = 0; q < g.n_peers; ++q) {
+              Out* Pq = static_cast<Out*>(g.peer_C[q]);
+              if (col0 < g.N) Pq[row * g.ldc + col0] = v[0];
+              if (col0 + 1 < g.N) Pq[row * g.ldc + col0 + 1] = v[1];
+            }
+          }
         }
       }
   }
+  if constexpr ((EPI & kEpiPeers) != 0) __threadfence_system();  // peer stores visible before completion
   if (__any_sync(0xffffffffu, changed) && lane == 0) atomicOr(&g.flags[BTAS_FLAG_CHANGED], 1);
   if (__any_sync(0xffffffffu, diag_neg) && lane == 0) atomicOr(&g.flags[BTAS_FLAG_DIAG_NEG], 1);
   if (P::kChecked) {
@@ -556,7 +576,15 @@ int launch_gemm_epi(const GemmArgs& g, cudaStream_t stream) {
 
 template <class P, bool MIN>
 int launch_tropical_gemm(const GemmArgs& g, cudaStream_t stream) {
-  switch ((g.Z != nullptr ? kEpiAcc : 0) | (g.Cprev != nullptr ? kEpiCmp : 0)) {
+  const int epi = (g.Z != nullptr ? kEpiAcc : 0) | (g.Cprev != nullptr ? kEpiCmp : 0);
+  if (g.n_peers > 0) {
+    // peer-store variants: the squaring step (compare against Cprev) and the plain product
+    if (g.n_peers > kMaxPeers) return BTAS_ERR_UNSUPPORTED;
+    if (epi == kEpiCmp) return launch_gemm_epi<P, MIN, kEpiCmp | kEpiPeers>(g, stream);
+    if (epi == kEpiPlain) return launch_gemm_epi<P, MIN, kEpiPlain | kEpiPeers>(g, stream);
+    return BTAS_ERR_UNSUPPORTED;
+  }
+  switch (epi) {
     case kEpiPlain:
       return launch_gemm_epi<P, MIN, kEpiPlain>(g, stream);
     case kEpiAcc:

@@ -6,9 +6,9 @@ namespace btas {
 BTAS_GEMM_DRIVER_DECL(float, gemm_f32) {
   const gemm_impl::WsLayout L = gemm_impl::ws_layout(Traits<float>::dtype, M, N, K);
   return min_plus ? gemm_impl::gemm_typed<float, true>(integer_mode, A, lda, B, ldb, Z, ldz, C, ldc, M, N, K, Cprev,
-                                                      ldcp, flags, ws, L, st)
+                                                      ldcp, flags, ws, L, peers, n_peers, st)
                   : gemm_impl::gemm_typed<float, false>(integer_mode, A, lda, B, ldb, Z, ldz, C, ldc, M, N, K, Cprev,
-                                                       ldcp, flags, ws, L, st);
+                                                       ldcp, flags, ws, L, peers, n_peers, st);
 }
 
 size_t gemm_ws_total(int dtype, int64_t M, int64_t N, int64_t K) {

@@ -6,9 +6,9 @@ namespace btas {
 BTAS_GEMM_DRIVER_DECL(double, gemm_f64) {
   const gemm_impl::WsLayout L = gemm_impl::ws_layout(Traits<double>::dtype, M, N, K);
   return min_plus ? gemm_impl::gemm_typed<double, true>(integer_mode, A, lda, B, ldb, Z, ldz, C, ldc, M, N, K, Cprev,
-                                                      ldcp, flags, ws, L, st)
+                                                      ldcp, flags, ws, L, peers, n_peers, st)
                   : gemm_impl::gemm_typed<double, false>(integer_mode, A, lda, B, ldb, Z, ldz, C, ldc, M, N, K, Cprev,
-                                                       ldcp, flags, ws, L, st);
+                                                       ldcp, flags, ws, L, peers, n_peers, st);
 }
 
 }  // namespace btas

@@ -6,9 +6,9 @@ namespace btas {
 BTAS_GEMM_DRIVER_DECL(int32_t, gemm_i32) {
   const gemm_impl::WsLayout L = gemm_impl::ws_layout(Traits<int32_t>::dtype, M, N, K);
   return min_plus ? gemm_impl::gemm_typed<int32_t, true>(integer_mode, A, lda, B, ldb, Z, ldz, C, ldc, M, N, K, Cprev,
-                                                      ldcp, flags, ws, L, st)
+                                                      ldcp, flags, ws, L, peers, n_peers, st)
                   : gemm_impl::gemm_typed<int32_t, false>(integer_mode, A, lda, B, ldb, Z, ldz, C, ldc, M, N, K, Cprev,
-                                                       ldcp, flags, ws, L, st);
+                                                       ldcp, flags, ws, L, peers, n_peers, st);
 }
 
 }  // namespace btas

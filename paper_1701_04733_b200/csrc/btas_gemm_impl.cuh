@@ -319,7 +319,7 @@ __global__ void pack_b_kernel(const T* __restrict__ B, int64_t ldb, int64_t K, i
 template <class T, bool MIN>
 int gemm_typed(int integer_mode, const T* A, int64_t lda, const T* B, int64_t ldb, const T* Z, int64_t ldz, T* C,
                int64_t ldc, int64_t M, int64_t N, int64_t K, const T* Cprev, int64_t ldcp, int32_t* flags,
-               unsigned char* ws, const WsLayout& L, cudaStream_t st) {
+               unsigned char* ws, const WsLayout& L, void* const* peers, int n_peers, cudaStream_t st) {
   using G = GemmGeometry<T>;
   constexpr bool kIsF64 = Traits<T>::dtype == BTAS_F64;
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(ws + L.ctrl);
@@ -373,6 +373,8 @@ int gemm_typed(int integer_mode, const T* A, int64_t lda, const T* B, int64_t ld
     g.gate = &ctrl->path;
     g.integer_mode = int_mode ? 1 : 0;
     g.limit = int_mode ? limit : INFINITY;
+    g.n_peers = n_peers;
+    for (int q = 0; q < n_peers && q < kMaxPeers; ++q) g.peer_C[q] = peers[q];
   }
   GemmArgs g16{};  // int16x2 path (integer operands with |x| < 2^12)
   const int bn16 = 32 * s16_gn();
@@ -433,7 +435,7 @@ int gemm_typed(int integer_mode, const T* A, int64_t lda, const T* B, int64_t ld
 #define BTAS_GEMM_DRIVER_DECL(T, NAME)                                                                       \
   int NAME(bool min_plus, int integer_mode, const T* A, int64_t lda, const T* B, int64_t ldb, const T* Z,      \
            int64_t ldz, T* C, int64_t ldc, int64_t M, int64_t N, int64_t K, const T* Cprev, int64_t ldcp,      \
-           int32_t* flags, unsigned char* ws, cudaStream_t st)
+           int32_t* flags, unsigned char* ws, void* const* peers, int n_peers, cudaStream_t st)
 BTAS_GEMM_DRIVER_DECL(float, gemm_f32);
 BTAS_GEMM_DRIVER_DECL(int32_t, gemm_i32);
 BTAS_GEMM_DRIVER_DECL(double, gemm_f64);

@@ -23,6 +23,7 @@ tile shape is a compile-time property of the kernels.
 
 from __future__ import annotations
 
+import ctypes
 import math
 import os
 import threading
@@ -531,8 +532,10 @@ def ew_add(a, b):
 
 
 def _gemm(x: torch.Tensor, y: torch.Tensor, kind: SemiringKind, integer: bool, *, z: "torch.Tensor | None" = None,
-          out: "torch.Tensor | None" = None, cprev: "torch.Tensor | None" = None) -> "tuple[torch.Tensor, torch.Tensor]":
-    """One btas_gemm call on the current stream; returns (C, flags)."""
+          out: "torch.Tensor | None" = None, cprev: "torch.Tensor | None" = None,
+          peers: "list[int] | None" = None) -> "tuple[torch.Tensor, torch.Tensor]":
+    """One btas_gemm call on the current stream; returns (C, flags).  ``peers``
+    (device addresses, same layout as ``out``) selects btas_gemm_peers."""
     m, k = x.shape
     n = y.shape[1]
     dev = x.device
@@ -542,14 +545,26 @@ def _gemm(x: torch.Tensor, y: torch.Tensor, kind: SemiringKind, integer: bool, *
     code = _dtype_code(x.dtype)
     nbytes = _lib.load().btas_gemm_workspace_bytes(code, m, n, k)
     ws = _workspace.get(dev, nbytes)
-    _lib.call(
-        "btas_gemm", code, _kind_code(kind), 1 if integer else 0,
-        _ptr(x), x.stride(0), _ptr(y), y.stride(0),
-        _ptr(z) if z is not None else None, z.stride(0) if z is not None else 0,
-        _ptr(out), out.stride(0), m, n, k,
-        _ptr(cprev) if cprev is not None else None, cprev.stride(0) if cprev is not None else 0,
-        _ptr(flags), _ptr(ws), ws.numel(), _stream(dev),
-    )
+    if peers:
+        # fused all-gather: the epilogue also stores C into each peer buffer
+        if z is not None:
+            raise ValueError("peer stores are not combined with accumulate_into")
+        arr = (ctypes.c_void_p * len(peers))(*peers)
+        _lib.call(
+            "btas_gemm_peers", code, _kind_code(kind), 1 if integer else 0,
+            _ptr(x), x.stride(0), _ptr(y), y.stride(0), _ptr(out), out.stride(0), m, n, k,
+            _ptr(cprev) if cprev is not None else None, cprev.stride(0) if cprev is not None else 0,
+            arr, len(peers), _ptr(flags), _ptr(ws), ws.numel(), _stream(dev),
+        )
+    else:
+        _lib.call(
+            "btas_gemm", code, _kind_code(kind), 1 if integer else 0,
+            _ptr(x), x.stride(0), _ptr(y), y.stride(0),
+            _ptr(z) if z is not None else None, z.stride(0) if z is not None else 0,
+            _ptr(out), out.stride(0), m, n, k,
+            _ptr(cprev) if cprev is not None else None, cprev.stride(0) if cprev is not None else 0,
+            _ptr(flags), _ptr(ws), ws.numel(), _stream(dev),
+        )
     _flags.track(flags)
     return out, flags
 

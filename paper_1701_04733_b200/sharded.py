@@ -14,7 +14,20 @@ Extends ``apsp_by_squaring`` (reference apsp.py:136-178) to P ranks of a
 
 The exchange volume per step is (P-1)/P * n^2 * 4 bytes per rank (≈15 GB at
 n = 65536 fp32, ≈20 ms over NVLink 5) against ≈n^3/P pairs of compute, so
-the all-gather is <2 % of a step; it is issued on the compute stream.
+the all-gather is <2 % of a step.
+
+Two exchanges are implemented:
+  * "peer" (default on NCCL when symmetric memory is available): D and D_next
+    live in torch symmetric memory (every rank maps every peer's buffers
+    over NVLink); btas_gemm_peers writes each finished output tile into the
+    rank's own D_next AND into the same rows of every peer's D_next from the
+    GEMM epilogue, so the all-gather disappears into the tile stores and
+    overlaps the compute tile by tile.  The flag all_reduce that ends every
+    step doubles as the barrier: a rank enters it only after its GEMM (which
+    ends with a system-scope fence) has completed, and it starts the next
+    step — which overwrites the buffer its peers read in this one — only
+    after every rank has entered it.
+  * "nccl": GEMM into the local rows, then all_gather_into_tensor.
 
 ``gemm_rows`` is injectable so the host-side logic (partition, collectives,
 loop control, probe) is testable with the gloo backend on CPU
@@ -40,6 +53,7 @@ class ShardedResult:
     negative_cycle: bool
     multiplications_performed: int
     saturated: bool
+    exchange: str = "nccl"
 
 
 def apsp_by_squaring_distributed(adj, group=None):
@@ -54,8 +68,7 @@ def apsp_by_squaring_distributed(adj, group=None):
 
     n = _require_square_minplus(adj)
     base = _closure_base(adj)
-    res = apsp_by_squaring_sharded(base.data.contiguous(), group=group,
-                                   gemm_rows=_cuda_gemm_rows(True, base.integer), integer=base.integer)
+    res = apsp_by_squaring_sharded(base.data.contiguous(), group=group, integer=base.integer)
     if res.saturated:
         _note_saturation()
     dist_m = TropicalMatrix._wrap(adj.kind, res.distances.contiguous(), base.integer)
@@ -81,8 +94,8 @@ def _cuda_gemm_rows(kind_min: bool, integer: bool) -> Callable:
 
     kind = SemiringKind.MIN_PLUS if kind_min else SemiringKind.MAX_PLUS
 
-    def gemm_rows(a_rows: torch.Tensor, b: torch.Tensor, cprev: torch.Tensor, out: torch.Tensor):
-        _, flags = _gemm(a_rows, b, kind, integer, out=out, cprev=cprev)
+    def gemm_rows(a_rows: torch.Tensor, b: torch.Tensor, cprev: torch.Tensor, out: torch.Tensor, peers=None):
+        _, flags = _gemm(a_rows, b, kind, integer, out=out, cprev=cprev, peers=peers)
         return torch.stack([flags[_lib.FLAG_CHANGED], flags[_lib.FLAG_DIAG_NEG], flags[_lib.FLAG_SATURATED]])
 
     return gemm_rows
@@ -98,21 +111,60 @@ def _diag_rows(d_rows: torch.Tensor, r0: int) -> torch.Tensor:
     return (diag < 0).any().to(torch.int32)
 
 
+def _peer_buffers(shape, dtype, dev, group, world):
+    """Two symmetric-memory buffers and, per buffer, the base addresses of
+    the other ranks' copies; None when symmetric memory is unavailable."""
+    try:
+        import torch.distributed._symmetric_memory as symm_mem
+
+        bufs, ptrs = [], []
+        me = dist.get_rank(group)
+        for _ in range(2):
+            t = symm_mem.empty(*shape, dtype=dtype, device=dev)
+            h = symm_mem.rendezvous(t, group if group is not None else dist.group.WORLD)
+            addrs = [int(a) for a in h.buffer_ptrs]
+            if len(addrs) != world or addrs[me] != t.data_ptr():
+                return None
+            bufs.append(t)
+            ptrs.append([a for q, a in enumerate(addrs) if q != me])
+        return bufs, ptrs
+    except Exception:  # no NVLink P2P / no symmetric-memory backend
+        return None
+
+
+def _want_peer_exchange(group, world: int, dev: torch.device) -> bool:
+    import os
+
+    # auto: fused when there is someone to exchange with; peer: always (the
+    # one-rank test of the symmetric-memory plumbing); nccl: never
+    mode = os.environ.get("BTAS_EXCHANGE", "auto")
+    if mode == "nccl" or world - 1 > 7 or dev.type != "cuda" or (world < 2 and mode != "peer"):
+        return False
+    return dist.get_backend(group) == "nccl"
+
+
 def apsp_by_squaring_sharded(base: torch.Tensor, group=None, gemm_rows: "Callable | None" = None,
                              integer: bool = True, align: int = 128) -> ShardedResult:
     """Closure of the closure base ``base`` (n x n oriented min-plus storage,
     identical on every rank) by repeated squaring, row-sharded over the
     group.  Mirrors apsp.py:136-178 step for step (fixpoint exit, counted
-    detecting square, uncounted probe)."""
+    detecting square, uncounted probe).  With the default CUDA ``gemm_rows``
+    on NCCL the exchange is fused into the GEMM epilogue (see module doc)."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     n = base.shape[0]
     dev = base.device
+    fused_ok = gemm_rows is None and _want_peer_exchange(group, world, dev)
     gemm_rows = gemm_rows or _cuda_gemm_rows(True, integer)
     chunk, spans = partition(n, world, align)
     r0, r1 = spans[rank]
 
-    bufs = [torch.empty((world * chunk, n), dtype=base.dtype, device=dev) for _ in range(2)]
+    peer = _peer_buffers((world * chunk, n), base.dtype, dev, group, world) if fused_ok else None
+    if peer is not None:
+        bufs, peer_ptrs = peer
+        row_off = r0 * n * base.element_size()
+    else:
+        bufs = [torch.empty((world * chunk, n), dtype=base.dtype, device=dev) for _ in range(2)]
     bufs[0][:n].copy_(base)
     cur = 0
     mults, fixpoint, sat = 0, False, False
@@ -123,10 +175,16 @@ def apsp_by_squaring_sharded(base: torch.Tensor, group=None, gemm_rows: "Callabl
         power = 1
         while power < n - 1:
             d, nxt = bufs[cur], bufs[1 - cur]
-            flags = gemm_rows(d[r0:r1], d[:n], d[r0:r1], nxt[r0:r1]) if r1 > r0 else \
-                torch.zeros(FLAG_WORDS, dtype=torch.int32, device=dev)
-            my_chunk = nxt[rank * chunk : (rank + 1) * chunk]
-            dist.all_gather_into_tensor(nxt, my_chunk, group=group)
+            if peer is not None:
+                # my rows land in every peer's D_next from the epilogue
+                peers = [a + row_off for a in peer_ptrs[1 - cur]]
+                flags = gemm_rows(d[r0:r1], d[:n], d[r0:r1], nxt[r0:r1], peers=peers) if r1 > r0 else \
+                    torch.zeros(FLAG_WORDS, dtype=torch.int32, device=dev)
+            else:
+                flags = gemm_rows(d[r0:r1], d[:n], d[r0:r1], nxt[r0:r1]) if r1 > r0 else \
+                    torch.zeros(FLAG_WORDS, dtype=torch.int32, device=dev)
+                my_chunk = nxt[rank * chunk : (rank + 1) * chunk]
+                dist.all_gather_into_tensor(nxt, my_chunk, group=group)
             flags = flags.to(torch.int32)
             dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=group)
             f = flags.cpu().tolist()
@@ -157,7 +215,72 @@ def apsp_by_squaring_sharded(base: torch.Tensor, group=None, gemm_rows: "Callabl
         f = flags.cpu().tolist()
         sat |= bool(f[2])
         negative = bool(f[0]) or bool(f[1])
-    return ShardedResult(res_d, negative, mults, sat)
+    return ShardedResult(res_d, negative, mults, sat, "peer" if peer is not None else "nccl")
+
+
+def apsp_by_squaring_emulated(adj, world: int):
+    """The fused peer-store squaring of ``apsp_by_squaring_sharded`` with
+    ``world`` virtual ranks on ONE GPU, run one after another on one stream:
+    each virtual rank owns its own D / D_next pair and its GEMM stores its
+    rows into every other virtual rank's D_next through btas_gemm_peers,
+    exactly the addresses the multi-GPU path uses.  Used by the GPU tests to
+    check the fused exchange bit for bit; returns (ApspReport, per-rank D)."""
+    from .apsp import Algorithm, ApspReport, DistanceMatrix, _closure_base, _require_square_minplus
+    from .matrix import TropicalMatrix
+
+    n = _require_square_minplus(adj)
+    base = _closure_base(adj)
+    b = base.data.contiguous()
+    dev = b.device
+    gemm_rows = _cuda_gemm_rows(True, base.integer)
+    chunk, spans = partition(n, world)
+    bufs = [[torch.empty((world * chunk, n), dtype=b.dtype, device=dev) for _ in range(2)] for _ in range(world)]
+    for r in range(world):
+        bufs[r][0][:n].copy_(b)
+    esz = b.element_size()
+    cur, mults, fixpoint, sat = 0, 0, False, False
+    power = 1
+    while n > 1 and power < n - 1:
+        flags = torch.zeros(FLAG_WORDS, dtype=torch.int32, device=dev)
+        for r, (r0, r1) in enumerate(spans):
+            if r1 <= r0:
+                continue
+            d, nxt = bufs[r][cur], bufs[r][1 - cur]
+            peers = [bufs[q][1 - cur].data_ptr() + r0 * n * esz for q in range(world) if q != r]
+            flags = torch.maximum(flags, gemm_rows(d[r0:r1], d[:n], d[r0:r1], nxt[r0:r1], peers=peers).to(torch.int32))
+        f = flags.cpu().tolist()
+        mults += 1
+        sat |= bool(f[2])
+        if not f[0]:
+            fixpoint = True
+            break
+        cur = 1 - cur
+        power *= 2
+    per_rank = [bufs[r][cur][:n] for r in range(world)]
+    d = per_rank[0]
+    if n == 1:
+        negative = bool((b < 0).any().item())  # probe I ⊗ base = base
+        d = torch.zeros_like(b)  # identity of size 1
+        per_rank = [d] * world
+    elif fixpoint:
+        negative = any(bool(_diag_rows(d[r0:r1], r0).item()) for r0, r1 in spans if r1 > r0)
+    else:
+        negative = False
+        for r0, r1 in spans:
+            if r1 <= r0:
+                continue
+            probe = torch.empty((r1 - r0, n), dtype=b.dtype, device=dev)
+            fl = gemm_rows(d[r0:r1], b, d[r0:r1], probe)
+            negative |= bool(fl[0].item()) or bool(_diag_rows(probe, r0).item())
+            sat |= bool(fl[2].item())
+    if sat:
+        from .semiring import _note_saturation
+
+        _note_saturation()
+    dist_m = TropicalMatrix._wrap(adj.kind, d.contiguous(), base.integer)
+    rep = ApspReport(distances=DistanceMatrix(n, dist_m), algorithm=Algorithm.REPEATED_SQUARING,
+                     negative_cycle=negative, multiplications_performed=mults)
+    return rep, per_rank
 
 
 # ---------------------------------------------------------------------------

@@ -196,12 +196,16 @@ def test_input_errors(cuda):
         bt.DistanceMatrix(3, bt.identity_matrix(MIN, 2))
 
 
-def test_sharded_squaring_nccl_single_rank(cuda):
-    """The distributed squaring path (NCCL all-gather + flag all-reduce, CUDA
-    row-block GEMM) on a one-rank group: identical to apsp_by_squaring."""
+@pytest.mark.parametrize("exchange", ["nccl", "peer"])
+def test_sharded_squaring_nccl_single_rank(cuda, exchange, monkeypatch):
+    """The distributed squaring path (NCCL all-gather or the symmetric-memory
+    peer-store exchange + flag all-reduce, CUDA row-block GEMM) on a one-rank
+    group: identical to apsp_by_squaring."""
     import torch.distributed as dist
 
-    from paper_1701_04733_b200.sharded import apsp_by_squaring_distributed
+    from paper_1701_04733_b200.sharded import apsp_by_squaring_distributed, apsp_by_squaring_sharded
+
+    monkeypatch.setenv("BTAS_EXCHANGE", exchange)
 
     created = False
     if not dist.is_initialized():
@@ -217,6 +221,8 @@ def test_sharded_squaring_nccl_single_rank(cuda):
             assert got.multiplications_performed == want.multiplications_performed
             if not want.negative_cycle:
                 assert got.distances.dist == want.distances.dist
+        base = bt.TropicalMatrix(MIN, [[0, 1], [1, 0]], dtype=torch.int32).data
+        assert apsp_by_squaring_sharded(base, integer=True).exchange == exchange
     finally:
         if created:
             dist.destroy_process_group()
