@@ -8,7 +8,7 @@ product path (btas_gemm: screen, packing, GEMM kernel) with A, B resident in
 HBM.  Metric: G(add,min)/s = n^3 / step time / 1e9.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
-                    [--workload gemm|gemm_f32|gemm_f32_real|fw|apsp] [--n N]
+                    [--workload gemm|gemm_f32|gemm_f32_real|fw|apsp|matvec|ewadd|graph] [--n N]
 
 N > 1 (launched by torchrun, one rank per GPU): every rank runs its own
 independent GEMM of the same size — the GEMM shards into independent output
@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="gemm",
-                    choices=["gemm", "gemm_f32", "gemm_f32_real", "fw", "apsp", "matvec", "ewadd"])
+                    choices=["gemm", "gemm_f32", "gemm_f32_real", "fw", "apsp", "matvec", "ewadd", "graph"])
     ap.add_argument("--batch", type=int, default=1, help="vectors per matvec (config C5: 1, 2, 4, 8)")
     ap.add_argument("--n", type=int, default=0, help="problem size (default per workload)")
     ap.add_argument("--no-variants", action="store_true")
@@ -184,6 +184,8 @@ def main():
         return apsp_arm(args, rank, world, dev)
     if args.workload in ("matvec", "ewadd"):
         return hbm_arm(args, rank, world, dev)
+    if args.workload == "graph":
+        return graph_arm(args, rank, world, dev)
 
     import paper_1701_04733_b200 as bt
     from paper_1701_04733_b200 import _lib
@@ -563,6 +565,61 @@ def hbm_arm(args, rank, world, dev):
                         "frac": round(gbs / hbm, 4), "traffic": None,
                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, read+write)"},
            "clocks": clocks.summary()}
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    return 0
+
+
+def graph_arm(args, rank, world, dev):
+    """On-device instance generation: the C3 instance
+    graph_to_matrix(random_graph(n, 0.5, (1, 100), instance_seed(1, n))) as
+    int32 storage, through the public random_graph_matrix (presence, draw and
+    fill kernels plus two 8-byte host reads).  HBM-bound on the matrix write
+    and the draw array round trip; the host restatement (numpy PCG64,
+    dense_rows) is timed beside it on a row sample."""
+    import torch
+
+    from paper_1701_04733_b200.graphs import dense_rows, instance_seed, random_graph_matrix
+
+    n = args.n or 32768
+    seed = instance_seed(1, n)
+    fn = lambda: random_graph_matrix(n, 0.5, (1, 100), seed, dtype=torch.int32, device=dev)  # noqa: E731
+    for _ in range(max(3, args.warmup)):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(int(dev.index)) as clocks:
+        s.record()
+        for _ in range(args.steps):
+            m = fn()
+        e.record()
+        torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / args.steps
+    edges = int((m.data < (1 << 28)).sum().item()) - n
+    nbytes = n * n * 4 + edges * 4 * 2  # matrix write + draw array write and read
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    res = {"metric": f"instance generation n={n} G entries/s", "value": round(n * n / (ms * 1e-3) / 1e9, 2),
+           "unit": "G entries/s", "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
+           "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "i32", "data": "synthetic",
+           "config": {"workload": f"random_graph_n{n}_i32", "graph": "random_graph p=0.5 weights 1..100",
+                      "edges": edges, "bytes_per_step": nbytes, "l2": "matrix >> L2"},
+           "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
+                        "frac": round(gbs / hbm, 4), "traffic": None,
+                        "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, read+write)",
+                        "note": "also ALU-bound: 2.5 n^2 PCG64 128-bit steps per instance"},
+           "clocks": clocks.summary()}
+    if rank == 0 and world == 1:
+        rows = 256
+        t = time.perf_counter()
+        for _ in dense_rows(n, 0.5, (1, 100), seed, chunk_rows=rows):
+            break
+        cpu_s = (time.perf_counter() - t) * n / rows
+        res["cpu_baseline"] = {"value": round(n * n / cpu_s / 1e9, 4), "unit": "G entries/s", "cores": 1,
+                               "kind": "port", "sample": f"first {rows} rows of the instance via dense_rows "
+                               "(numpy PCG64 + scatter), extrapolated to n rows"}
     if rank == 0:
         print(json.dumps(res), flush=True)
     return 0

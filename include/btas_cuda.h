@@ -216,6 +216,53 @@ int btas_diag_negative(int dtype, const void* d, int64_t ld, int64_t n, int32_t*
  * SM clock (MHz) of the run.  Synchronises (diagnostic only). */
 int btas_probe_ceiling(int mix, double* pairs_per_clk_sm, double* sm_mhz, double* tpairs_per_s);
 
+/* ---------------------------------------------------------------------------
+ * On-device instance generator: replaces random_graph + graph_to_matrix
+ * (reference graph_io.py:273-304, 158-165) for dense instances.
+ *
+ * The reference draws from ONE numpy PCG64 stream (XSL-RR 128/64, the
+ * state after SeedSequence seeding is passed in as btas_pcg64): first one
+ * uniform double per ordered off-diagonal pair in row-major order
+ * (present iff (u >> 11) < p_threshold, p_threshold = ceil(p * 2^53)), then
+ * one weight per present edge:
+ *   BTAS_WEIGHTS_CONST    integers(low, low+1): no draws, weight = low
+ *   BTAS_WEIGHTS_BOUNDED  integers(low, low+range+1): Lemire bounded draws on
+ *                         the 32-bit-buffered stream (range < 2^32) or on the
+ *                         64-bit stream (range >= 2^32), with numpy's rejection
+ *   BTAS_WEIGHTS_UNIFORM  uniform(low, low+scale): low + scale * double
+ * and builds the dense min-plus matrix (diagonal 0, absent edges +inf,
+ * converted and validated exactly as btas_ingest does from float64).
+ *
+ * Three stream-ordered stages; the caller reads the edge count written by
+ * stage 1 to size the draw buffer, and the accepted-draw count written by
+ * stage 2 to decide whether another window of draws is needed (only bounded
+ * draws reject).  Draw buffer elements: uint32 (range < 2^32), uint64
+ * (range >= 2^32) or double (uniform).
+ * ------------------------------------------------------------------------- */
+typedef struct btas_pcg64 {
+  uint64_t state_hi, state_lo, inc_hi, inc_lo;
+} btas_pcg64;
+
+enum { BTAS_WEIGHTS_CONST = 0, BTAS_WEIGHTS_BOUNDED = 1, BTAS_WEIGHTS_UNIFORM = 2 };
+
+/* workspace of all three stages for an n-vertex instance */
+size_t btas_graph_workspace_bytes(int64_t n);
+/* stage 1 (random_graph presence draws): *dev_edges (device int64) = number of present pairs */
+int btas_graph_presence(const btas_pcg64* rng, int64_t n, uint64_t p_threshold, void* workspace,
+                        size_t workspace_bytes, int64_t* dev_edges, btas_stream_t stream);
+/* stage 2 (weight draws): consumes the 64-bit stream units [unit0, unit0 + units) past the
+ * presence doubles, appends accepted draws with rank < edges to draws[], and advances
+ * *dev_accepted (device int64, 0 before the first window).  units <= n*(n-1) + 2^20. */
+int btas_graph_draw(const btas_pcg64* rng, int64_t n, int weights_mode, uint64_t range, double low,
+                    double scale, int64_t edges, uint64_t unit0, uint64_t units, void* draws,
+                    void* workspace, size_t workspace_bytes, int64_t* dev_accepted, btas_stream_t stream);
+/* stage 3 (graph_to_matrix): dense n x n min-plus storage of dtype into D (leading dim ld);
+ * reuses stage 1's counts in the workspace; stats as btas_ingest reports them. */
+int btas_graph_fill(int dtype, const btas_pcg64* rng, int64_t n, uint64_t p_threshold, int weights_mode,
+                    uint64_t range, int64_t low, const void* draws, void* D, int64_t ld,
+                    const void* workspace, size_t workspace_bytes, btas_stats* stats_dev,
+                    btas_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,10 +66,21 @@ class Stats(ctypes.Structure):
 
 STATS_WORDS = 9  # 64-bit words of btas_stats
 
+
+class Pcg64(ctypes.Structure):
+    """btas_pcg64 (include/btas_cuda.h): a numpy PCG64 state."""
+
+    _fields_ = [("state_hi", ctypes.c_uint64), ("state_lo", ctypes.c_uint64), ("inc_hi", ctypes.c_uint64),
+                ("inc_lo", ctypes.c_uint64)]
+
+
+WEIGHTS_CONST, WEIGHTS_BOUNDED, WEIGHTS_UNIFORM = 0, 1, 2
+
 _p = ctypes.c_void_p
 _i64 = ctypes.c_int64
 _i32 = ctypes.c_int
 _sz = ctypes.c_size_t
+_u64 = ctypes.c_uint64
 _dbl = ctypes.c_double
 
 # name -> (restype, argtypes); the exact export list of include/btas_cuda.h
@@ -104,6 +115,12 @@ SIGNATURES = {
     "btas_fw_dist_stage": (_i32, [_i32, _i32, _i32, _p, _i64, _i64, _i64, _i64, _i64, _i32, _dbl, _p, _p, _sz, _p]),
     "btas_diag_negative": (_i32, [_i32, _p, _i64, _i64, _p, _p]),
     "btas_probe_ceiling": (_i32, [_i32, ctypes.POINTER(_dbl), ctypes.POINTER(_dbl), ctypes.POINTER(_dbl)]),
+    "btas_graph_workspace_bytes": (_sz, [_i64]),
+    "btas_graph_presence": (_i32, [ctypes.POINTER(Pcg64), _i64, _u64, _p, _sz, _p, _p]),
+    "btas_graph_draw": (_i32, [ctypes.POINTER(Pcg64), _i64, _i32, _u64, _dbl, _dbl, _i64, _u64, _u64, _p, _p, _sz, _p,
+                               _p]),
+    "btas_graph_fill": (_i32, [_i32, ctypes.POINTER(Pcg64), _i64, _u64, _i32, _u64, _i64, _p, _p, _i64, _p, _sz, _p,
+                               _p]),
 }
 
 _lock = threading.Lock()

@@ -1,5 +1,9 @@
 """Seeded random dense digraphs straight into device storage.
 
+``random_graph_matrix`` generates the instance on the GPU (btas_graph_*
+kernels, csrc/btas_graph.cu); ``dense_rows`` / ``random_graph_matrix_host``
+are the host restatement used as its independent check.
+
 A vectorised, chunked restatement of the reference instance generator
 ``random_graph`` + ``graph_to_matrix`` (btas/graph_io.py:273-304,158-165) and
 of ``instance_seed`` (btas/bench.py:153-156): the same PCG64 streams in the
@@ -16,6 +20,7 @@ presence doubles.
 
 from __future__ import annotations
 
+import ctypes
 import math
 
 import numpy as np
@@ -86,9 +91,86 @@ def dense_rows(n: int, p: float, weight_range, seed: int, chunk_rows: int = 1024
         yield r0, block
 
 
+def pcg64_state(seed: int) -> "_lib.Pcg64":
+    """numpy's PCG64(seed) state after SeedSequence seeding (graph_io.py:289)."""
+    st = np.random.PCG64(int(seed) & 0xFFFF_FFFF_FFFF_FFFF).state["state"]
+    m64 = (1 << 64) - 1
+    return _lib.Pcg64(st["state"] >> 64, st["state"] & m64, st["inc"] >> 64, st["inc"] & m64)
+
+
+def _weight_plan(low: float, high: float):
+    """(mode, range, int offset, float low, scale) of the reference weight draw
+    (graph_io.py:300-303): integers(low, high + 1) or uniform(low, high)."""
+    if low.is_integer() and high.is_integer():
+        lo, hi = int(low), int(high)
+        if lo < -(1 << 63) or hi + 1 > (1 << 63):
+            raise ValueError(f"integer weight range ({low!r}, {high!r}) exceeds int64")
+        rng = hi - lo
+        return (_lib.WEIGHTS_CONST if rng == 0 else _lib.WEIGHTS_BOUNDED), rng, lo, 0.0, 0.0
+    scale = high - low
+    if not math.isfinite(scale):
+        raise OverflowError("Range exceeds valid bounds")  # numpy Generator.uniform
+    return _lib.WEIGHTS_UNIFORM, 0, 0, low, scale
+
+
 def random_graph_matrix(n: int, p: float, weight_range, seed: int, *, dtype: "torch.dtype | None" = None,
-                        device=None, chunk_rows: int = 1024) -> TropicalMatrix:
-    """The reference instance as a min-plus TropicalMatrix on the GPU."""
+                        device=None) -> TropicalMatrix:
+    """The reference instance ``graph_to_matrix(random_graph(n, p, weight_range,
+    seed))`` generated on the GPU (include/btas_cuda.h btas_graph_*): presence
+    draws, weight draws and the dense fill run as CUDA kernels over the same
+    PCG64 stream, so the matrix is bit-identical to the reference's (and to
+    ``dense_rows``) with no host-side O(n^2) work.  Two small host reads:
+    the edge count and the accepted-draw count."""
+    p, low, high = _check(n, p, weight_range)
+    dt = dtype if dtype is not None else get_default_dtype()
+    dev = _resolve_device(device)
+    code = _dtype_code(dt)
+    rng = pcg64_state(seed)
+    thr = math.ceil(p * 2.0**53)  # u >> 11 < thr  <=>  (u >> 11) * 2^-53 < p  (exact)
+    mode, wrange, off, flow, scale = _weight_plan(low, high)
+    lib = _lib.load()
+    ws = torch.empty(max(1, lib.btas_graph_workspace_bytes(n)), dtype=torch.uint8, device=dev)
+    edges_t = torch.zeros(1, dtype=torch.int64, device=dev)
+    s = _stream(dev)
+    _lib.call("btas_graph_presence", ctypes.byref(rng), n, thr, _ptr(ws), ws.numel(), _ptr(edges_t), s)
+    edges = int(edges_t.item())
+    draws = None
+    if mode != _lib.WEIGHTS_CONST and edges > 0:
+        if mode == _lib.WEIGHTS_UNIFORM:
+            draws, per_unit, accept = torch.empty(edges, dtype=torch.float64, device=dev), 1, 1.0
+        elif wrange < 0xFFFF_FFFF:
+            draws, per_unit = torch.empty(edges, dtype=torch.int32, device=dev), 2
+            accept = 1.0 - ((0xFFFF_FFFF - wrange) % (wrange + 1)) / 2.0**32
+        elif wrange == 0xFFFF_FFFF:
+            draws, per_unit, accept = torch.empty(edges, dtype=torch.int32, device=dev), 2, 1.0
+        else:
+            draws, per_unit = torch.empty(edges, dtype=torch.int64, device=dev), 1
+            accept = 1.0 - ((0xFFFF_FFFF_FFFF_FFFF - wrange) % (wrange + 1)) / 2.0**64
+        acc_t = torch.zeros(1, dtype=torch.int64, device=dev)
+        unit0, accepted = 0, 0
+        cap = n * (n - 1) + (1 << 20)
+        while accepted < edges:
+            need = edges - accepted
+            units = min(cap, math.ceil(need / (per_unit * accept) * 1.001) + 4096)
+            _lib.call("btas_graph_draw", ctypes.byref(rng), n, mode, wrange, flow, scale, edges, unit0, units,
+                      _ptr(draws), _ptr(ws), ws.numel(), _ptr(acc_t), s)
+            unit0 += units
+            accepted = int(acc_t.item())
+    out = torch.empty((n, n), dtype=dt, device=dev)
+    stats = _new_stats(dev)
+    _lib.call("btas_graph_fill", code, ctypes.byref(rng), n, thr, mode, wrange, off,
+              _ptr(draws) if draws is not None else None, _ptr(out), n, _ptr(ws), ws.numel(), _ptr(stats), s)
+    st = _read_stats(stats)
+    if st.out_of_range:
+        raise ValueError(f"instance weights do not fit {dt} storage")
+    integer = dt == torch.int32 or (st.non_integral == 0 and st.over_limit == 0)
+    return TropicalMatrix._wrap(SemiringKind.MIN_PLUS, out, integer)
+
+
+def random_graph_matrix_host(n: int, p: float, weight_range, seed: int, *, dtype: "torch.dtype | None" = None,
+                             device=None, chunk_rows: int = 1024) -> TropicalMatrix:
+    """The same instance through the host restatement ``dense_rows`` (numpy's
+    own PCG64) and btas_ingest: the independent check of the device generator."""
     dt = dtype if dtype is not None else get_default_dtype()
     dev = _resolve_device(device)
     out = torch.empty((n, n), dtype=dt, device=dev)
