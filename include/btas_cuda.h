@@ -263,6 +263,17 @@ int btas_graph_fill(int dtype, const btas_pcg64* rng, int64_t n, uint64_t p_thre
                     const void* workspace, size_t workspace_bytes, btas_stats* stats_dev,
                     btas_stream_t stream);
 
+/* graph_to_matrix of an explicit edge list (reference graph_io.py:158-165 with
+ * the Graph normalisation of :64-83: duplicate (src, dst) keep the minimum
+ * weight, -0.0 -> +0.0): D = +inf off the diagonal, 0 on it, then every edge
+ * min-scattered (a negative self-loop lowers the diagonal).  dev_errors
+ * (device int64[3]) receives the smallest failing edge index per class, or m
+ * when none fails: [0] src/dst outside [0, n), [1] non-finite weight,
+ * [2] weight not representable in dtype (int32: integral, |w| < 2^28).
+ * Statistics of the result: btas_scan. */
+int btas_edges_to_matrix(int dtype, int64_t n, const int64_t* src, const int64_t* dst, const double* weight,
+                         int64_t m, void* D, int64_t ld, int64_t* dev_errors, btas_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -116,6 +116,7 @@ SIGNATURES = {
     "btas_diag_negative": (_i32, [_i32, _p, _i64, _i64, _p, _p]),
     "btas_probe_ceiling": (_i32, [_i32, ctypes.POINTER(_dbl), ctypes.POINTER(_dbl), ctypes.POINTER(_dbl)]),
     "btas_graph_workspace_bytes": (_sz, [_i64]),
+    "btas_edges_to_matrix": (_i32, [_i32, _i64, _p, _p, _p, _i64, _p, _i64, _p, _p]),
     "btas_graph_presence": (_i32, [ctypes.POINTER(Pcg64), _i64, _u64, _p, _sz, _p, _p]),
     "btas_graph_draw": (_i32, [ctypes.POINTER(Pcg64), _i64, _i32, _u64, _dbl, _dbl, _i64, _u64, _u64, _p, _p, _sz, _p,
                                _p]),

@@ -313,6 +313,106 @@ __global__ void __launch_bounds__(kGenThreads) fill_kernel(const __grid_constant
   commit(st, stats);
 }
 
+// ------------------------------------------------------------------ edge lists
+// graph_to_matrix of an explicit edge list (graph_io.py:158-165 after the
+// Graph normalisation of :64-83): +inf, diagonal 0, then min-scatter of every
+// edge.  The scatter is an atomicMin on an order-preserving integer image of
+// the stored value, so duplicates and self-loops resolve exactly as the
+// reference's "keep the minimum" in any order.
+BTAS_D uint32_t f32_key(float x) {
+  const uint32_t b = __float_as_uint(x);
+  return (b >> 31) ? ~b : (b | 0x80000000u);
+}
+BTAS_D float key_f32(uint32_t k) { return __uint_as_float((k >> 31) ? (k & 0x7FFFFFFFu) : ~k); }
+
+enum { kErrIndex = 0, kErrWeight = 1, kErrRange = 2, kErrWords = 3 };
+
+template <class D>
+__global__ void edges_init_kernel(D* __restrict__ out, int64_t n, int64_t ld, int64_t m, int64_t* err) {
+  if (blockIdx.x == 0 && threadIdx.x < kErrWords) err[threadIdx.x] = m;  // m: no failing edge
+  const int64_t total = n * n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / n, c = i - r * n;
+    D* p = out + r * ld + c;
+    if constexpr (Traits<D>::dtype == BTAS_F64) {
+      *reinterpret_cast<unsigned long long*>(p) = f64_key(r == c ? 0.0 : (double)INFINITY);
+    } else if constexpr (Traits<D>::dtype == BTAS_F32) {
+      *reinterpret_cast<uint32_t*>(p) = f32_key(r == c ? 0.0f : INFINITY);
+    } else {
+      *p = r == c ? 0 : kI32Inf;
+    }
+  }
+}
+
+template <class D>
+__global__ void edges_scatter_kernel(D* __restrict__ out, int64_t n, int64_t ld, const int64_t* __restrict__ src,
+                                     const int64_t* __restrict__ dst, const double* __restrict__ w, int64_t m,
+                                     int64_t* err) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = src[e], b = dst[e];
+    if (a < 0 || a >= n || b < 0 || b >= n) {
+      atomicMin(reinterpret_cast<unsigned long long*>(err + kErrIndex), (unsigned long long)e);
+      continue;
+    }
+    double x = w[e];
+    if (!isfinite(x)) {
+      atomicMin(reinterpret_cast<unsigned long long*>(err + kErrWeight), (unsigned long long)e);
+      continue;
+    }
+    x = x + 0.0;  // -0.0 -> +0.0 (graph_io.py:78-79)
+    D* p = out + a * ld + b;
+    if constexpr (Traits<D>::dtype == BTAS_F64) {
+      atomicMin(reinterpret_cast<unsigned long long*>(p), f64_key(x));
+    } else if constexpr (Traits<D>::dtype == BTAS_F32) {
+      const float f = (float)x;  // rounding is monotone: min then round == round then min
+      if (isinf(f)) {
+        atomicMin(reinterpret_cast<unsigned long long*>(err + kErrRange), (unsigned long long)e);
+        continue;
+      }
+      atomicMin(reinterpret_cast<uint32_t*>(p), f32_key(f));
+    } else {
+      if (x != floor(x) || fabs(x) >= (double)kI32Limit) {
+        atomicMin(reinterpret_cast<unsigned long long*>(err + kErrRange), (unsigned long long)e);
+        continue;
+      }
+      atomicMin(reinterpret_cast<int*>(p), (int)x);
+    }
+  }
+}
+
+template <class D>
+__global__ void edges_decode_kernel(D* __restrict__ out, int64_t n, int64_t ld) {
+  const int64_t total = n * n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / n, c = i - r * n;
+    D* p = out + r * ld + c;
+    if constexpr (Traits<D>::dtype == BTAS_F64) {
+      *p = key_f64(*reinterpret_cast<unsigned long long*>(p));
+    } else {
+      *p = key_f32(*reinterpret_cast<uint32_t*>(p));
+    }
+  }
+}
+
+template <class D>
+int edges_typed(int64_t n, const int64_t* src, const int64_t* dst, const double* w, int64_t m, D* out, int64_t ld,
+                int64_t* err, cudaStream_t st) {
+  const unsigned cap = (unsigned)device_sm_count() * 8;
+  const unsigned g_nn = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n * n, 256), cap));
+  edges_init_kernel<D><<<g_nn, 256, 0, st>>>(out, n, ld, m, err);
+  BTAS_CUDA_CHECK_LAUNCH();
+  if (m > 0) {
+    const unsigned g_m = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, 256), cap));
+    edges_scatter_kernel<D><<<g_m, 256, 0, st>>>(out, n, ld, src, dst, w, m, err);
+    BTAS_CUDA_CHECK_LAUNCH();
+  }
+  if constexpr (Traits<D>::dtype != BTAS_I32) {
+    edges_decode_kernel<D><<<g_nn, 256, 0, st>>>(out, n, ld);
+    BTAS_CUDA_CHECK_LAUNCH();
+  }
+  return BTAS_OK;
+}
+
 // ------------------------------------------------------------------ host
 struct GraphWs {
   int32_t *p_warp, *p_cta, *d_warp, *d_cta;
@@ -471,4 +571,20 @@ extern "C" int btas_graph_fill(int dtype, const btas_pcg64* rng, int64_t n, uint
   }
   BTAS_CUDA_CHECK_LAUNCH();
   return BTAS_OK;
+}
+
+extern "C" int btas_edges_to_matrix(int dtype, int64_t n, const int64_t* src, const int64_t* dst, const double* weight,
+                                    int64_t m, void* D, int64_t ld, int64_t* dev_errors, btas_stream_t stream) {
+  if (n < 1 || m < 0 || !D || ld < n || !dev_errors || (m > 0 && (!src || !dst || !weight))) return BTAS_ERR_INVALID;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  switch (dtype) {
+    case BTAS_F32:
+      return edges_typed<float>(n, src, dst, weight, m, static_cast<float*>(D), ld, dev_errors, st);
+    case BTAS_I32:
+      return edges_typed<int32_t>(n, src, dst, weight, m, static_cast<int32_t*>(D), ld, dev_errors, st);
+    case BTAS_F64:
+      return edges_typed<double>(n, src, dst, weight, m, static_cast<double*>(D), ld, dev_errors, st);
+    default:
+      return BTAS_ERR_INVALID;
+  }
 }

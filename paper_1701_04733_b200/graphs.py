@@ -186,3 +186,60 @@ def random_graph_matrix_host(n: int, p: float, weight_range, seed: int, *, dtype
         raise ValueError(f"instance weights do not fit {dt} storage")
     integer = dt == torch.int32 or (st.non_integral == 0 and st.over_limit == 0)
     return TropicalMatrix._wrap(kind, out, integer)
+
+
+def edges_to_matrix(n: int, src, dst, weight, *, dtype: "torch.dtype | None" = None, device=None) -> TropicalMatrix:
+    """``graph_to_matrix`` (graph_io.py:158-165) of an edge list given as three
+    equal-length arrays (numpy or torch; src/dst integer, weight float):
+    +inf off the diagonal, 0 on it, duplicates keep the minimum weight and a
+    negative self-loop lowers the diagonal (Graph normalisation,
+    graph_io.py:64-83).  One init, one atomic min-scatter and one decode
+    kernel (btas_edges_to_matrix); errors are raised with the reference's
+    messages for the first offending edge."""
+    if not isinstance(n, int) or n < 1:
+        raise ValueError(f"vertex count must be a positive integer, got {n!r}")
+    dt = dtype if dtype is not None else get_default_dtype()
+    dev = _resolve_device(device)
+
+    def dev_arr(a, tdt):
+        t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(np.asarray(a)))
+        return t.to(device=dev, dtype=tdt).contiguous().reshape(-1)
+
+    s_t, d_t, w_t = dev_arr(src, torch.int64), dev_arr(dst, torch.int64), dev_arr(weight, torch.float64)
+    m = s_t.numel()
+    if d_t.numel() != m or w_t.numel() != m:
+        raise ValueError("src, dst and weight must have the same length")
+    out = torch.empty((n, n), dtype=dt, device=dev)
+    err = torch.empty(3, dtype=torch.int64, device=dev)
+    s = _stream(dev)
+    _lib.call("btas_edges_to_matrix", _dtype_code(dt), n, _ptr(s_t), _ptr(d_t), _ptr(w_t), m, _ptr(out), n,
+              _ptr(err), s)
+    stats = _new_stats(dev)
+    _lib.call("btas_scan", _dtype_code(dt), _ptr(out), out.numel(), _ptr(stats), s)
+    e_index, e_weight, e_range = (int(v) for v in err.cpu().tolist())
+    if min(e_index, e_weight) < m:
+        e = min(e_index, e_weight)
+        a, b = int(s_t[e].item()), int(d_t[e].item())
+        if e == e_index:
+            raise ValueError(f"edge ({a}, {b}) out of range for n={n}")
+        raise ValueError(f"edge ({a}, {b}) weight must be finite, got {float(w_t[e].item())!r}")
+    if e_range < m:
+        if dt == torch.int32:
+            raise ValueError(f"int32 storage needs integral entries with magnitude below {_lib.I32_LIMIT}")
+        raise ValueError(f"entries do not fit {dt} storage")
+    st = _read_stats(stats)
+    integer = dt == torch.int32 or (st.non_integral == 0 and st.over_limit == 0)
+    return TropicalMatrix._wrap(SemiringKind.MIN_PLUS, out, integer)
+
+
+def graph_to_matrix(g, *, dtype: "torch.dtype | None" = None, device=None) -> TropicalMatrix:
+    """graph_io.graph_to_matrix (graph_io.py:158-165) for a reference ``Graph``
+    (anything with ``.n`` and ``.edges`` = ((src, dst, weight), ...))."""
+    edges = tuple(g.edges)
+    if edges:
+        arr = np.asarray([(float(a), float(b), float(w)) for a, b, w in edges], dtype=np.float64)
+        src, dst, w = arr[:, 0].astype(np.int64), arr[:, 1].astype(np.int64), arr[:, 2]
+    else:
+        src = dst = np.zeros(0, dtype=np.int64)
+        w = np.zeros(0, dtype=np.float64)
+    return edges_to_matrix(int(g.n), src, dst, w, dtype=dtype, device=device)

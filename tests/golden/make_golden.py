@@ -169,6 +169,55 @@ def generator_digests():
     )
 
 
+def generator_families():
+    """random_graph weight families beyond the benchmark's (graph_io.py:300-303):
+    constant ranges, Lemire draws with frequent rejections, raw 32-bit words,
+    64-bit draws and zero-scale uniforms — digests of graph_to_matrix."""
+    cases = [(40, 0.5, (7, 7), 21), (90, 0.6, (0, 2**31), 22), (70, 0.5, (-(2**31), 2**31 - 1), 23),
+             (60, 0.7, (0, 2**32), 24), (50, 0.5, (-(2**62), 2**62), 25), (45, 0.5, (2.5, 2.5), 26),
+             (33, 1.0, (-1000.0, 1000.5), 27), (20, 0.0, (1, 100), 28)]
+    out = []
+    for n, p, wr, s in cases:
+        adj = ref.graph_to_matrix(ref.random_graph(n, p, wr, s))
+        out.append(digest(adj.data))
+    np.savez_compressed(
+        HERE / "generator_families.npz",
+        n=np.array([c[0] for c in cases]), p=np.array([c[1] for c in cases]),
+        lo=np.array([c[2][0] for c in cases], dtype=np.float64), hi=np.array([c[2][1] for c in cases], dtype=np.float64),
+        seed=np.array([c[3] for c in cases]), digest=np.array(out),
+    )
+
+
+def edgelist_cases():
+    """graph_to_matrix of explicit edge lists (graph_io.py:64-83,158-165):
+    duplicate pairs (minimum kept), self-loops of both signs, -0.0 weights and
+    real weights; the reference Graph normalises, graph_to_matrix scatters."""
+    rng = random.Random(0xED6E)
+    arrays = {}
+    count = 40
+    for case in range(count):
+        n = rng.randint(1, 24)
+        m = rng.randint(0, 3 * n * n)
+        src = [rng.randrange(n) for _ in range(m)]
+        dst = [rng.randrange(n) for _ in range(m)]
+        if case % 4 == 3:
+            w = [rng.uniform(-5, 50) for _ in range(m)]
+        else:
+            w = [float(rng.randint(-4, 40)) for _ in range(m)]
+        for i in range(0, m, 7):
+            w[i] = -0.0 if w[i] == 0 else w[i]
+        g = ref.Graph(n=n, edges=tuple(zip(src, dst, w)))
+        adj = ref.graph_to_matrix(g)
+        arrays[f"n{case}"] = np.array([n])
+        arrays[f"src{case}"] = np.array(src, dtype=np.int64)
+        arrays[f"dst{case}"] = np.array(dst, dtype=np.int64)
+        arrays[f"w{case}"] = np.array(w, dtype=np.float64)
+        arrays[f"out{case}"] = compact(adj.data)
+        arrays[f"integer{case}"] = np.array([int(adj.integer)])
+    arrays["count"] = np.array([count])
+    np.savez_compressed(HERE / "edgelist.npz", **arrays)
+
+
 def kat_cases():
     """Known answers of the reference tests (test_matrix.py, test_apsp.py),
     recomputed on the reference."""
@@ -249,6 +298,8 @@ def main():
     mult_count_cases()
     c1_case()
     generator_digests()
+    generator_families()
+    edgelist_cases()
     kat_cases()
     for f in sorted(HERE.glob("*.npz")):
         print(f"{f.name}: {f.stat().st_size / 1024:.1f} KiB")

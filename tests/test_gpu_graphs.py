@@ -90,3 +90,89 @@ def test_validation_errors(cuda):
     for gen in (random_graph_matrix, random_graph_matrix_host):
         with pytest.raises(ValueError):
             gen(4, 0.5, (-1.5e308, 1.5e308), 1)
+
+
+def _digest(t):
+    import hashlib
+
+    import numpy as np
+
+    return hashlib.sha256(np.ascontiguousarray(t, dtype=np.float64).tobytes()).hexdigest()
+
+
+def test_device_generator_reference_digests(cuda, golden):
+    """float64 storage of the device generator == the reference's bytes."""
+    for name in ("generator.npz", "generator_families.npz"):
+        g = golden(name)
+        for i in range(len(g["n"])):
+            n, p, wr, seed = int(g["n"][i]), float(g["p"][i]), (g["lo"][i], g["hi"][i]), int(g["seed"][i])
+            adj = random_graph_matrix(n, p, wr, seed, dtype=torch.float64)
+            assert _digest(adj.to_numpy()) == str(g["digest"][i]), (name, i)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32, torch.int32])
+def test_edge_list_matches_reference(cuda, golden, dtype):
+    import numpy as np
+
+    from oracle import graphs as og
+    from paper_1701_04733_b200.graphs import edges_to_matrix
+
+    g = golden("edgelist.npz")
+    for case in range(int(g["count"][0])):
+        n = int(g[f"n{case}"][0])
+        src, dst, w = g[f"src{case}"], g[f"dst{case}"], g[f"w{case}"]
+        want = np.asarray(g[f"out{case}"], dtype=np.float64)
+        integral = bool(g[f"integer{case}"][0])
+        if dtype == torch.int32 and not integral:
+            with pytest.raises(ValueError):
+                edges_to_matrix(n, src, dst, w, dtype=dtype)
+            continue
+        got = edges_to_matrix(n, src, dst, w, dtype=dtype)
+        if dtype == torch.float64:
+            assert got.to_numpy().tobytes() == want.tobytes(), case
+            assert got.integer == integral
+        else:
+            assert got.to_numpy().tobytes() == want.astype(np.float32).astype(np.float64).tobytes(), case
+        # torch inputs on the device take the same path
+        t = edges_to_matrix(n, torch.as_tensor(src, device="cuda"), torch.as_tensor(dst, device="cuda"),
+                            torch.as_tensor(w, device="cuda"), dtype=dtype)
+        assert torch.equal(t.data, got.data)
+        assert og.graph_to_matrix_edges(n, src, dst, w).astype(np.float64).tobytes() == want.tobytes()
+
+
+def test_edge_list_errors_and_graph_objects(cuda):
+    import numpy as np
+
+    from paper_1701_04733_b200.graphs import edges_to_matrix, graph_to_matrix
+    from oracle.graphs import graph_to_matrix_edges
+
+    with pytest.raises(ValueError, match=r"edge \(0, 3\) out of range for n=3"):
+        edges_to_matrix(3, [0, 0], [1, 3], [1.0, 2.0])
+    with pytest.raises(ValueError, match=r"edge \(1, 1\) weight must be finite"):
+        edges_to_matrix(3, [0, 1], [1, 1], [1.0, math.inf])
+    with pytest.raises(ValueError):
+        edges_to_matrix(0, [], [], [])
+    with pytest.raises(ValueError):
+        edges_to_matrix(3, [0], [1, 2], [1.0])
+
+    class G:  # duck-typed reference Graph
+        n = 4
+        edges = ((0, 1, 5.0), (0, 1, 3.0), (2, 2, -1.0), (3, 0, -0.0), (1, 1, 7.0))
+
+    got = graph_to_matrix(G(), dtype=torch.float64)
+    want = graph_to_matrix_edges(4, [0, 0, 2, 3, 1], [1, 1, 2, 0, 1], [5.0, 3.0, -1.0, -0.0, 7.0])
+    assert got.to_numpy().tobytes() == want.tobytes() and got.integer
+
+    class E:
+        n = 2
+        edges = ()
+
+    assert graph_to_matrix(E(), dtype=torch.int32).to_numpy().tobytes() == \
+        np.array([[0.0, math.inf], [math.inf, 0.0]]).tobytes()
+    # the edge list of a generated instance rebuilds the same matrix
+    adj = random_graph_matrix(300, 0.2, (-5, 40), 77, dtype=torch.float32)
+    d = adj.data
+    mask = torch.isfinite(d) & ~torch.eye(300, dtype=torch.bool, device=d.device)
+    s, t = mask.nonzero(as_tuple=True)
+    back = edges_to_matrix(300, s, t, d[s, t].double(), dtype=torch.float32)
+    assert torch.equal(back.data, d) and back.integer == adj.integer

@@ -231,6 +231,36 @@ def test_generator_matches_reference(golden):
             assert digest(adj) == str(g["digest"][i]), (n, chunk)
 
 
+def test_generator_families_match_reference(golden):
+    """Constant, rejection-heavy, raw-32, 64-bit and uniform weight families:
+    the one-shot oracle restatement and the chunked host generator both
+    reproduce the reference's graph_to_matrix(random_graph(...)) bytes."""
+    from oracle import graphs as og
+    from paper_1701_04733_b200.graphs import dense_rows
+
+    for name in ("generator.npz", "generator_families.npz"):
+        g = golden(name)
+        for i in range(len(g["n"])):
+            n, p, wr, seed = int(g["n"][i]), float(g["p"][i]), (g["lo"][i], g["hi"][i]), int(g["seed"][i])
+            assert digest(og.random_graph_dense(n, p, wr, seed)) == str(g["digest"][i]), (name, i)
+            adj = np.concatenate([b for _, b in dense_rows(n, p, wr, seed, chunk_rows=5)])
+            assert digest(adj) == str(g["digest"][i]), (name, i)
+
+
+def test_edge_list_oracle_matches_reference(golden):
+    from oracle import graphs as og
+
+    g = golden("edgelist.npz")
+    for case in range(int(g["count"][0])):
+        n = int(g[f"n{case}"][0])
+        got = og.graph_to_matrix_edges(n, g[f"src{case}"], g[f"dst{case}"], g[f"w{case}"])
+        assert got.tobytes() == f64(g[f"out{case}"]).tobytes(), case
+    with pytest.raises(ValueError, match="out of range"):
+        og.graph_to_matrix_edges(3, [0, 3], [1, 1], [1.0, 2.0])
+    with pytest.raises(ValueError, match="finite"):
+        og.graph_to_matrix_edges(3, [0, 1], [1, 1], [1.0, math.nan])
+
+
 def test_c_oracle_fw_matches_numpy():
     rng = random.Random(3)
     for _ in range(10):
