@@ -90,6 +90,12 @@ const char* btas_version(void);
 const char* btas_status_string(int status);
 /* decode an ordered key of btas_stats; returns NaN for the "no finite entry" key */
 double btas_key_to_double(unsigned long long key);
+/* Copy `words` 32-bit words (<= 4096) from device memory to `dst` with SM
+ * stores, where dst may be page-locked host memory (cudaHostAlloc'd, mapped
+ * under unified addressing).  The host reads small results (stats, flag words)
+ * this way so the read never queues behind an unrelated bulk device->host copy
+ * on the copy engine; the caller synchronises on an event after the call. */
+int btas_export_words(const void* src, void* dst, int64_t words, btas_stream_t stream);
 /* reset a device btas_stats before an ingest/scan */
 int btas_stats_init(btas_stats* stats_dev, btas_stream_t stream);
 

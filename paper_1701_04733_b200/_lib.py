@@ -89,6 +89,7 @@ SIGNATURES = {
     "btas_status_string": (ctypes.c_char_p, [_i32]),
     "btas_key_to_double": (_dbl, [ctypes.c_ulonglong]),
     "btas_stats_init": (_i32, [_p, _p]),
+    "btas_export_words": (_i32, [_p, _p, _i64, _p]),
     "btas_ingest": (_i32, [_i32, _i32, _p, _i64, _i32, _p, _p, _p]),
     "btas_scan": (_i32, [_i32, _p, _i64, _p, _p]),
     "btas_to_f64": (_i32, [_i32, _p, _i64, _p, _p]),

@@ -410,6 +410,23 @@ extern "C" double btas_key_to_double(unsigned long long key) {
   return key_f64(key);
 }
 
+namespace btas {
+namespace {
+__global__ void export_words_kernel(const uint32_t* __restrict__ src, volatile uint32_t* dst, int64_t words) {
+  for (int64_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+}
+}  // namespace
+}  // namespace btas
+
+extern "C" int btas_export_words(const void* src, void* dst, int64_t words, btas_stream_t stream) {
+  if (!src || !dst || words < 0 || words > 4096) return BTAS_ERR_INVALID;
+  if (words == 0) return BTAS_OK;
+  btas::export_words_kernel<<<1, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint32_t*>(src), static_cast<volatile uint32_t*>(dst), words);
+  BTAS_CUDA_CHECK_LAUNCH();
+  return BTAS_OK;
+}
+
 extern "C" int btas_stats_init(btas_stats* s, btas_stream_t stream) {
   if (!s) return BTAS_ERR_INVALID;
   stats_init_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(s);

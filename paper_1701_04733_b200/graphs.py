@@ -30,6 +30,7 @@ from . import _lib
 from .matrix import (
     TropicalMatrix,
     _dtype_code,
+    _host_read,
     _kind_code,
     _new_stats,
     _ptr,
@@ -133,7 +134,7 @@ def random_graph_matrix(n: int, p: float, weight_range, seed: int, *, dtype: "to
     edges_t = torch.zeros(1, dtype=torch.int64, device=dev)
     s = _stream(dev)
     _lib.call("btas_graph_presence", ctypes.byref(rng), n, thr, _ptr(ws), ws.numel(), _ptr(edges_t), s)
-    edges = int(edges_t.item())
+    edges = int(_host_read(edges_t)[0])
     draws = None
     if mode != _lib.WEIGHTS_CONST and edges > 0:
         if mode == _lib.WEIGHTS_UNIFORM:
@@ -155,7 +156,7 @@ def random_graph_matrix(n: int, p: float, weight_range, seed: int, *, dtype: "to
             _lib.call("btas_graph_draw", ctypes.byref(rng), n, mode, wrange, flow, scale, edges, unit0, units,
                       _ptr(draws), _ptr(ws), ws.numel(), _ptr(acc_t), s)
             unit0 += units
-            accepted = int(acc_t.item())
+            accepted = int(_host_read(acc_t)[0])
     out = torch.empty((n, n), dtype=dt, device=dev)
     stats = _new_stats(dev)
     _lib.call("btas_graph_fill", code, ctypes.byref(rng), n, thr, mode, wrange, off,
@@ -216,7 +217,7 @@ def edges_to_matrix(n: int, src, dst, weight, *, dtype: "torch.dtype | None" = N
               _ptr(err), s)
     stats = _new_stats(dev)
     _lib.call("btas_scan", _dtype_code(dt), _ptr(out), out.numel(), _ptr(stats), s)
-    e_index, e_weight, e_range = (int(v) for v in err.cpu().tolist())
+    e_index, e_weight, e_range = (int(v) for v in _host_read(err))
     if min(e_index, e_weight) < m:
         e = min(e_index, e_weight)
         a, b = int(s_t[e].item()), int(d_t[e].item())

@@ -188,10 +188,14 @@ class _FlagLedger:
     def read_saturation(self) -> bool:
         with self._lock:
             pending, self._pending = self._pending, []
-        seen = False
+        by_dev: "dict[torch.device, list[torch.Tensor]]" = {}
         for f in pending:
-            if int(f[_lib.FLAG_SATURATED].item()) != 0:
-                seen = True
+            by_dev.setdefault(f.device, []).append(f)
+        seen = False
+        for dev, fs in by_dev.items():
+            with torch.cuda.device(dev):
+                sat = torch.stack([f[_lib.FLAG_SATURATED] for f in fs]).amax().reshape(1)
+                seen |= int(_host_read(sat)[0]) != 0
         return seen
 
     def reset(self) -> None:
@@ -203,8 +207,48 @@ _flags = _FlagLedger()
 _register_device_flags(_flags.read_saturation, _flags.reset)
 
 
+class _HostReader:
+    """Small device results (stats, flag words, counts) read through a
+    page-locked host buffer written by SM stores (btas_export_words), not by a
+    device-to-host copy: a copy would queue on the copy engine behind any bulk
+    download another stream has in flight (a pipelined caller's result
+    transfer), stalling every validation read for its duration."""
+
+    _CAP = 16384
+
+    def __init__(self):
+        self._tls = threading.local()
+
+    def read(self, t: torch.Tensor) -> np.ndarray:
+        t = t.detach().contiguous()
+        nbytes = t.numel() * t.element_size()
+        np_dtype = torch.empty(0, dtype=t.dtype).numpy().dtype
+        if nbytes == 0:
+            return np.zeros(t.shape, dtype=np_dtype)
+        if nbytes % 4 or nbytes > self._CAP or t.device.type != "cuda":
+            return t.cpu().numpy()
+        buf = getattr(self._tls, "buf", None)
+        if buf is None:
+            buf = torch.empty(self._CAP, dtype=torch.uint8, pin_memory=True)
+            self._tls.buf = buf
+        stream = torch.cuda.current_stream(t.device)
+        _lib.call("btas_export_words", t.data_ptr(), buf.data_ptr(), nbytes // 4, stream.cuda_stream)
+        done = torch.cuda.Event()
+        done.record(stream)
+        done.synchronize()
+        return buf[:nbytes].numpy().view(np_dtype).reshape(t.shape).copy()
+
+
+_host = _HostReader()
+
+
+def _host_read(t: torch.Tensor) -> np.ndarray:
+    """Synchronously read a small device tensor (see _HostReader)."""
+    return _host.read(t)
+
+
 def _read_stats(stats: torch.Tensor) -> _lib.Stats:
-    host = stats.cpu().numpy().view(np.uint64)
+    host = _host_read(stats).view(np.uint64)
     s = _lib.Stats()
     for i, (name, _) in enumerate(_lib.Stats._fields_):
         setattr(s, name, int(host[i]))

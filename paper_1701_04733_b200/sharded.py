@@ -43,6 +43,7 @@ import torch
 import torch.distributed as dist
 
 from . import _lib
+from .matrix import _host_read
 
 FLAG_WORDS = 3  # changed, diag_neg, saturated
 
@@ -187,7 +188,7 @@ def apsp_by_squaring_sharded(base: torch.Tensor, group=None, gemm_rows: "Callabl
                 dist.all_gather_into_tensor(nxt, my_chunk, group=group)
             flags = flags.to(torch.int32)
             dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=group)
-            f = flags.cpu().tolist()
+            f = _host_read(flags).tolist()
             mults += 1
             sat |= bool(f[2])
             if not f[0]:
@@ -212,7 +213,7 @@ def apsp_by_squaring_sharded(base: torch.Tensor, group=None, gemm_rows: "Callabl
         # diagonal of this row block here
         flags[1] = _diag_rows(probe_out, r0)
         dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=group)
-        f = flags.cpu().tolist()
+        f = _host_read(flags).tolist()
         sat |= bool(f[2])
         negative = bool(f[0]) or bool(f[1])
     return ShardedResult(res_d, negative, mults, sat, "peer" if peer is not None else "nccl")
@@ -248,7 +249,7 @@ def apsp_by_squaring_emulated(adj, world: int):
             d, nxt = bufs[r][cur], bufs[r][1 - cur]
             peers = [bufs[q][1 - cur].data_ptr() + r0 * n * esz for q in range(world) if q != r]
             flags = torch.maximum(flags, gemm_rows(d[r0:r1], d[:n], d[r0:r1], nxt[r0:r1], peers=peers).to(torch.int32))
-        f = flags.cpu().tolist()
+        f = _host_read(flags).tolist()
         mults += 1
         sat |= bool(f[2])
         if not f[0]:
@@ -407,7 +408,7 @@ def floyd_warshall_distributed(adj, group=None):
     if r1 > r0:
         mine[: r1 - r0].copy_(d[r0:r1])
     dist.all_gather_into_tensor(full, mine, group=group)
-    f = flags.cpu().tolist()
+    f = _host_read(flags).tolist()
     if f[_lib.FLAG_SATURATED]:
         _note_saturation()
     return _fw_report(adj, full[:n].contiguous() if world * chunk != n else full, bool(f[_lib.FLAG_DIAG_NEG]))

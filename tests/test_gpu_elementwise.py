@@ -153,3 +153,22 @@ def test_container_semantics(cuda):
     f = bt.TropicalMatrix.filled(MIN, 2, 3, 5)
     assert f.to_lists() == [[5] * 3] * 2
     assert "2x3" in repr(f)
+
+
+def test_host_read_small_results(cuda):
+    """btas_export_words: small device results reach the host through SM
+    stores into page-locked memory, bit for bit, for every word size."""
+    from paper_1701_04733_b200.matrix import _host_read
+
+    g = torch.Generator(device="cuda").manual_seed(3)
+    for dt in (torch.int32, torch.int64, torch.float32, torch.float64, torch.uint8):
+        for shape in ((1,), (9,), (3, 5), (4096,)):
+            t = torch.randint(-100, 100, shape, generator=g, device="cuda").to(dt)
+            got = _host_read(t)
+            assert got.dtype == t.cpu().numpy().dtype and got.shape == tuple(shape)
+            assert got.tobytes() == t.cpu().numpy().tobytes()
+    # non-contiguous and oversize inputs take the copy fallback
+    t = torch.arange(20000, device="cuda", dtype=torch.int32)
+    assert _host_read(t).tobytes() == t.cpu().numpy().tobytes()
+    assert _host_read(t[::3]).tobytes() == t[::3].cpu().numpy().tobytes()
+    assert _host_read(torch.zeros(0, device="cuda")).shape == (0,)
