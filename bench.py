@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-apsp", action="store_true", help="skip the APSP C4 measurement of the default run")
+    ap.add_argument("--apsp-n", type=int, default=65536, help="APSP C4 size inside the default run")
     return ap.parse_args()
 
 
@@ -323,11 +325,86 @@ def main():
                       "NumPy restatement of btas.matmul (_product_tile broadcast-add + reduce, thread pool of "
                       f"{cores} workers)",
         }
+    # ------------------------------------------------------------- APSP C4 (north-star scaling row)
+    if not args.no_apsp and args.workload == "gemm":
+        del x, y, out, xs, ys
+        torch.cuda.empty_cache()
+
+        def give_up():  # a stuck exchange must not cost the GEMM line
+            result["apsp_c4"] = {"error": f"timed out after {APSP_WATCHDOG_S} s"}
+            if rank == 0:
+                print(json.dumps(result), flush=True)
+            os._exit(0)
+
+        timer = threading.Timer(APSP_WATCHDOG_S, give_up)
+        timer.daemon = True
+        timer.start()
+        try:
+            result["apsp_c4"] = apsp_c4(args.apsp_n, rank, world, dev)
+        except Exception as exc:  # report, keep the GEMM line
+            result["apsp_c4"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        finally:
+            timer.cancel()
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+APSP_WATCHDOG_S = 420
+
+
+def apsp_c4(n, rank, world, dev):
+    """BASELINE config C4 inside the default run: repeated-squaring APSP of
+    the n = 65536 instance graph_to_matrix(random_graph(n, 0.5, (1, 100),
+    instance_seed(1, n))) in fp32, on 1 GPU or row-sharded over the ranks
+    (all-gather fused into the GEMM epilogue over symmetric memory, NCCL
+    fallback).  One timed solve after a small warm-up solve; device time,
+    max over ranks.  "scaling": strong (the instance is fixed)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1701_04733_b200 as bt
+    from paper_1701_04733_b200.graphs import instance_seed, random_graph_matrix
+
+    if world > 1:
+        from paper_1701_04733_b200.sharded import apsp_by_squaring_distributed as solver
+    else:
+        solver = bt.apsp_by_squaring
+    solver(random_graph_matrix(2048, 0.5, (1, 100), instance_seed(1, 2048), dtype=torch.float32, device=dev))
+    adj = random_graph_matrix(n, 0.5, (1, 100), instance_seed(1, n), dtype=torch.float32, device=dev)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    rep = solver(adj)
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    d = rep.distances.dist.data
+    checksum = 0  # of the finite distances (inf -> -1), identical for every N
+    for r0 in range(0, n, 4096):
+        blk = d[r0:r0 + 4096]
+        blk = torch.where(torch.isfinite(blk), blk, torch.full_like(blk, -1)).to(torch.int64)
+        checksum = (checksum + int(blk.sum().item())) % (1 << 61)
+    out = {"metric": f"APSP time n={n}", "value": round(ms / 1e3, 3), "unit": "s", "higher_is_better": False,
+           "n_gpus": world, "scaling": "strong", "dtype": "f32",
+           "config": {"workload": f"apsp_squaring_n{n}_f32", "graph": "random_graph p=0.5 weights 1..100",
+                      "instance_seed": "instance_seed(1, n)"},
+           "multiplications": rep.multiplications_performed, "negative_cycle": rep.negative_cycle,
+           "distance_checksum": checksum,
+           "tpairs_per_s": round(float(n) ** 3 * rep.multiplications_performed / (ms * 1e-3) / 1e12, 2)}
+    if world > 1:
+        out["exchange"] = os.environ.get("BTAS_EXCHANGE", "auto")
+    del adj, rep, d
+    torch.cuda.empty_cache()
+    return out
 
 
 def e2e_gemm(n, dtype, xs, ys, dev, steps):
