@@ -161,6 +161,11 @@ def apsp_by_squaring_sharded(base: torch.Tensor, group=None, gemm_rows: "Callabl
     r0, r1 = spans[rank]
 
     peer = _peer_buffers((world * chunk, n), base.dtype, dev, group, world) if fused_ok else None
+    if fused_ok:  # every rank must take the same exchange
+        ok = torch.tensor([1 if peer is not None else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if not int(_host_read(ok)[0]):
+            peer = None
     if peer is not None:
         bufs, peer_ptrs = peer
         row_off = r0 * n * base.element_size()
