@@ -222,6 +222,21 @@ int btas_diag_negative(int dtype, const void* d, int64_t ld, int64_t n, int32_t*
  * SM clock (MHz) of the run.  Synchronises (diagnostic only). */
 int btas_probe_ceiling(int mix, double* pairs_per_clk_sm, double* sm_mhz, double* tpairs_per_s);
 
+/* Repeated-squaring APSP (apsp.py:136-178) of a small graph in ONE
+ * cooperative kernel: every squaring, its fixpoint compare, the uncounted
+ * negative-cycle probe and the result copy run on the device with grid-wide
+ * barriers between dependent steps (no per-step host round trip).  base is
+ * the closure base I (+) A (min-plus storage, n x n, 2 <= n <=
+ * BTAS_APSP_SMALL_MAX_N); out receives the distances.  dev_result (device
+ * int32[4]): multiplications_performed, negative_cycle, saturated, fixpoint.
+ * The saturation bit is also ORed into dev_flags.  Results are identical to
+ * the btas_gemm-driven loop. */
+#define BTAS_APSP_SMALL_MAX_N 1024
+size_t btas_apsp_small_workspace_bytes(int dtype, int64_t n);
+int btas_apsp_squaring_small(int dtype, int integer_mode, const void* base, int64_t ldb, int64_t n,
+                             void* out, int64_t ldo, int32_t* dev_result, int32_t* dev_flags,
+                             void* workspace, size_t workspace_bytes, btas_stream_t stream);
+
 /* ---------------------------------------------------------------------------
  * On-device instance generator: replaces random_graph + graph_to_matrix
  * (reference graph_io.py:273-304, 158-165) for dense instances.

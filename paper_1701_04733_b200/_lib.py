@@ -34,6 +34,7 @@ PATH_NAMES = {
     PATH_EMPTY: "empty",
 }
 OK, ERR_INVALID, ERR_CUDA, ERR_WORKSPACE, ERR_UNSUPPORTED = 0, 1, 2, 3, 4
+APSP_SMALL_MAX_N = 1024
 
 
 class NativeLibraryMissing(RuntimeError):
@@ -116,6 +117,8 @@ SIGNATURES = {
     "btas_fw_dist_stage": (_i32, [_i32, _i32, _i32, _p, _i64, _i64, _i64, _i64, _i64, _i32, _dbl, _p, _p, _sz, _p]),
     "btas_diag_negative": (_i32, [_i32, _p, _i64, _i64, _p, _p]),
     "btas_probe_ceiling": (_i32, [_i32, ctypes.POINTER(_dbl), ctypes.POINTER(_dbl), ctypes.POINTER(_dbl)]),
+    "btas_apsp_small_workspace_bytes": (_sz, [_i32, _i64]),
+    "btas_apsp_squaring_small": (_i32, [_i32, _i32, _p, _i64, _i64, _p, _i64, _p, _p, _p, _sz, _p]),
     "btas_graph_workspace_bytes": (_sz, [_i64]),
     "btas_edges_to_matrix": (_i32, [_i32, _i64, _p, _p, _p, _i64, _p, _i64, _p, _p]),
     "btas_graph_presence": (_i32, [ctypes.POINTER(Pcg64), _i64, _u64, _p, _sz, _p, _p]),

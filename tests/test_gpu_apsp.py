@@ -226,3 +226,46 @@ def test_sharded_squaring_nccl_single_rank(cuda, exchange, monkeypatch):
     finally:
         if created:
             dist.destroy_process_group()
+
+
+def _both_paths(monkeypatch, adj):
+    monkeypatch.setenv("BTAS_APSP_SMALL_MAX_N", "0")
+    bt.reset_saturation()
+    want = bt.apsp_by_squaring(adj)
+    want_sat = bt.saturation_seen()
+    monkeypatch.delenv("BTAS_APSP_SMALL_MAX_N")
+    bt.reset_saturation()
+    got = bt.apsp_by_squaring(adj)
+    got_sat = bt.saturation_seen()
+    return want, want_sat, got, got_sat
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_small_graph_kernel_matches_general_path(cuda, dtype, monkeypatch):
+    """The one-kernel small-graph squaring (btas_apsp_squaring_small) against
+    the btas_gemm-driven loop: distances, count, negative cycle, saturation."""
+    rng = np.random.default_rng(17)
+    cases = [(2, 0.5, (1, 9)), (3, 1.0, (-2, 5)), (33, 0.3, (1, 100)), (257, 0.05, (0, 60)), (700, 0.5, (1, 100)),
+             (1024, 0.01, (1, 1000)), (130, 0.4, (-1, 40))]
+    for n, p, wr in cases:
+        adj = random_graph_matrix(n, p, wr, int(rng.integers(1 << 30)), dtype=dtype)
+        want, ws, got, gs = _both_paths(monkeypatch, adj)
+        assert got.multiplications_performed == want.multiplications_performed, n
+        assert got.negative_cycle == want.negative_cycle, n
+        assert ws == gs
+        if not want.negative_cycle:
+            assert got.distances.dist == want.distances.dist, n
+    # magnitudes that overflow: the masked-candidate variant and the flag
+    big = {torch.float64: 1e308, torch.float32: 3e38, torch.int32: 2**27 - 1}[dtype]
+    for n in (5, 70):
+        sym = rng.uniform(big / 2, big, (n, n))
+        if dtype != torch.float64:
+            sym = np.floor(sym) if dtype == torch.int32 else sym
+        sym[rng.random((n, n)) < 0.3] = math.inf
+        np.fill_diagonal(sym, 0.0)
+        adj = bt.TropicalMatrix(bt.SemiringKind.MIN_PLUS, sym, dtype=dtype)
+        want, ws, got, gs = _both_paths(monkeypatch, adj)
+        assert ws and gs
+        assert (got.multiplications_performed, got.negative_cycle) == (want.multiplications_performed,
+                                                                       want.negative_cycle)
+        assert got.distances.dist == want.distances.dist
