@@ -327,17 +327,236 @@ __global__ void __launch_bounds__(256) matvec_kernel(const T* __restrict__ A, in
   if (__any_sync(0xffffffffu, sat) && l == 0) atomicOr(&flags[BTAS_FLAG_SATURATED], 1);
 }
 
+// ---- many vectors (5-8) of 4-byte storage: one pass over A -----------------
+// With 8 vectors every A element feeds 8 add-min pairs, so the pass is only
+// HBM-bound if A streams with enough bytes in flight AND the vectors are not
+// re-read from L2 for every few rows.  CTA = 32 rows (warp w: rows 4w..4w+3);
+// per 256-column chunk each lane streams 4 rows x 2 float4 of A into
+// registers (two CTAs per SM) while the chunk's 8 vector slices (8 KB) sit in
+// shared memory, double-buffered with cp.async, so L2 sees each vector once
+// per 32 rows.  The pass is issue-bound (8 add-min pairs per A element), so
+// the finite-magnitude screen costs two integer ops per element (abs_key).  The exact overflow screen is the
+// one of matvec_kernel; a CTA whose screen fails recomputes its rows with the
+// masked candidates.
+constexpr int kWideRows = 32, kWideChunk = 256, kWideNB = 8, kWideThreads = 256;
+
+BTAS_D void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+BTAS_D void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+BTAS_D void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// max |finite| bookkeeping in one or two integer ops per element: the
+// tracked key is monotone in |x| for finite x and negative for the stored
+// Infinity, so a signed max ignores it.  f32: (|x| bits) + 2^23 (inf bits
+// become 0x80000000); i32: |x| << 2 (the int32 Inf encoding wraps negative).
+template <class T>
+BTAS_D int32_t abs_key(T x) {
+  if constexpr (Traits<T>::dtype == BTAS_F32) return (int32_t)((__float_as_uint(x) & 0x7FFFFFFFu) + 0x00800000u);
+  else return (int32_t)((uint32_t)abs(x) << 2);
+}
+template <class T>
+BTAS_D T key_abs(int32_t k) {
+  if constexpr (Traits<T>::dtype == BTAS_F32) return k <= 0 ? 0.0f : __uint_as_float((uint32_t)k - 0x00800000u);
+  else return (T)(k >> 2);
+}
+
+template <class T, bool MIN>
+__global__ void __launch_bounds__(kWideThreads, 2) matvec_wide_kernel(const T* __restrict__ A, int64_t lda, int64_t M,
+                                                                   int64_t K, const T* __restrict__ Vv, int64_t ldv,
+                                                                   int nb, T* __restrict__ Out, int64_t ldo,
+                                                                   int int_mode, double limit, int32_t* flags) {
+  static_assert(sizeof(T) == 4, "4-byte storage");
+  __shared__ __align__(16) T Vs[2][kWideNB][kWideChunk];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r0 = (int64_t)blockIdx.x * kWideRows;
+  const T eps = Traits<T>::eps(MIN);
+  const int64_t nchunks = K / kWideChunk;  // the caller guarantees K % kWideChunk == 0
+  // stage vector chunk c into buffer c & 1 (vectors past nb are eps)
+  auto stage = [&](int64_t c) {
+    T(*dst)[kWideChunk] = Vs[c & 1];
+    for (int e = threadIdx.x; e < kWideNB * kWideChunk / 4; e += kWideThreads) {
+      const int b = e / (kWideChunk / 4), q = e % (kWideChunk / 4);
+      if (b < nb) {
+        cp_async16(&dst[b][q * 4], Vv + (int64_t)b * ldv + c * kWideChunk + q * 4);
+      } else {
+        T* d = &dst[b][q * 4];
+        d[0] = d[1] = d[2] = d[3] = eps;
+      }
+    }
+    cp_async_commit();
+  };
+  T acc[4][kWideNB];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int b = 0; b < kWideNB; ++b) acc[r][b] = eps;
+  int32_t akey = 0, vkey = 0;
+  const T* arow[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int64_t row = r0 + warp * 4 + r;
+    arow[r] = A + (row < M ? row : M - 1) * lda;
+  }
+  stage(0);
+  for (int64_t c = 0; c < nchunks; ++c) {
+    uint4 av[4][kWideChunk / 128];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int j = 0; j < kWideChunk / 128; ++j)
+        av[r][j] = __ldcs(reinterpret_cast<const uint4*>(arow[r] + c * kWideChunk + j * 128 + lane * 4));
+    if (c + 1 < nchunks) {
+      stage(c + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const T(*vs)[kWideChunk] = Vs[c & 1];
+#pragma unroll
+    for (int j = 0; j < kWideChunk / 128; ++j) {
+      const int col = j * 128 + lane * 4;
+      T v[kWideNB][4];
+#pragma unroll
+      for (int b = 0; b < kWideNB; ++b) {
+        const uint4 u = *reinterpret_cast<const uint4*>(&vs[b][col]);
+        v[b][0] = __builtin_bit_cast(T, u.x);
+        v[b][1] = __builtin_bit_cast(T, u.y);
+        v[b][2] = __builtin_bit_cast(T, u.z);
+        v[b][3] = __builtin_bit_cast(T, u.w);
+        if (warp == 0) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) vkey = max(vkey, abs_key(v[b][e]));
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const T a[4] = {__builtin_bit_cast(T, av[r][j].x), __builtin_bit_cast(T, av[r][j].y),
+                        __builtin_bit_cast(T, av[r][j].z), __builtin_bit_cast(T, av[r][j].w)};
+        akey = max(akey, max(max(abs_key(a[0]), abs_key(a[1])), max(abs_key(a[2]), abs_key(a[3]))));
+#pragma unroll
+        for (int b = 0; b < kWideNB; ++b) {
+          if constexpr (Traits<T>::dtype == BTAS_F32) {
+#pragma unroll
+            for (int e = 0; e < 4; e += 2) {
+              const float2 s2 = __fadd2_rn(make_float2(a[e], a[e + 1]), make_float2(v[b][e], v[b][e + 1]));
+              acc[r][b] = MIN ? fminf(fminf(acc[r][b], s2.x), s2.y) : fmaxf(fmaxf(acc[r][b], s2.x), s2.y);
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              acc[r][b] = MIN ? __viaddmin_s32(a[e], v[b][e], acc[r][b]) : __viaddmax_s32(a[e], v[b][e], acc[r][b]);
+          }
+        }
+      }
+    }
+    __syncthreads();  // buffer c & 1 is restaged at iteration c + 1
+  }
+  T amax = key_abs<T>(akey), vmax = key_abs<T>(vkey);
+  // exact screen over the CTA (see matvec_kernel)
+  __shared__ T scratch[kWideThreads / 32];
+  amax = block_max(amax, scratch);
+  vmax = block_max(vmax, scratch);
+  bool possible;
+  if constexpr (Traits<T>::dtype == BTAS_I32) {
+    possible = (int64_t)amax + (int64_t)vmax >= (int64_t)kI32Limit;
+  } else {
+    const T bound = amax + vmax;
+    possible = int_mode ? ((double)bound >= limit) : isinf(bound);
+  }
+  if (!possible) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int64_t row = r0 + warp * 4 + r;
+#pragma unroll
+      for (int b = 0; b < kWideNB; ++b) {
+        T v = acc[r][b];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const T u = __shfl_xor_sync(0xffffffffu, v, o);
+          v = MIN ? (u < v ? u : v) : (u > v ? u : v);
+        }
+        if constexpr (Traits<T>::dtype == BTAS_I32) {
+          if (MIN ? v >= (T)kI32Limit : v <= -(T)kI32Limit) v = eps;
+        }
+        if (lane == 0 && row < M && b < nb) Out[(int64_t)b * ldo + row] = v;
+      }
+    }
+    return;
+  }
+  // rare: masked candidates, 4 rows at a time with the whole CTA over k
+  bool sat = false;
+  __shared__ T red[kWideThreads / 32][4 * kWideNB];
+  for (int g = 0; g < kWideRows / 4; ++g) {
+    const int64_t rg = r0 + g * 4;
+    if (rg >= M) break;
+    T acc4[4][kWideNB];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int b = 0; b < kWideNB; ++b) acc4[r][b] = eps;
+    T am = 0, vm = 0;
+    mv_pass<T, MIN, 4, kWideNB, true>(A, lda, M, K, Vv, ldv, nb, rg, (K / 4) * 4, int_mode, limit, acc4, am, vm,
+                                       sat);
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int b = 0; b < kWideNB; ++b) {
+        T v = acc4[r][b];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const T u = __shfl_xor_sync(0xffffffffu, v, o);
+          v = MIN ? (u < v ? u : v) : (u > v ? u : v);
+        }
+        if (lane == 0) red[warp][r * kWideNB + b] = v;
+      }
+    __syncthreads();
+    if (threadIdx.x < 4 * kWideNB) {
+      const int r = threadIdx.x / kWideNB, b = threadIdx.x % kWideNB;
+      T v = red[0][threadIdx.x];
+      for (int ww = 1; ww < kWideThreads / 32; ++ww) {
+        const T u = red[ww][threadIdx.x];
+        v = MIN ? (u < v ? u : v) : (u > v ? u : v);
+      }
+      if constexpr (Traits<T>::dtype == BTAS_I32) {
+        if (MIN ? v >= (T)kI32Limit : v <= -(T)kI32Limit) v = eps;
+      }
+      if (rg + r < M && b < nb) Out[(int64_t)b * ldo + rg + r] = v;
+    }
+    __syncthreads();
+  }
+  if (__any_sync(0xffffffffu, sat) && lane == 0) atomicOr(&flags[BTAS_FLAG_SATURATED], 1);
+}
+
 template <class T, bool MIN>
 int matvec_typed(int int_mode, const T* A, int64_t lda, int64_t M, int64_t K, const T* V, int64_t ldv,
                  int64_t batch, T* Out, int64_t ldo, int32_t* flags, cudaStream_t st) {
   const double limit = Traits<T>::dtype == BTAS_I32 ? (double)kI32Limit : Traits<T>::int_limit;
-  // up to 4 vectors per pass over A: with more, the per-element add-min
-  // work outweighs the HBM stream (measured: 8 vectors in one pass ran at
-  // 2.1 TB/s, two passes of 4 at twice the rate)
-  for (int64_t b0 = 0; b0 < batch; b0 += 4) {
-    const int nb = (int)std::min<int64_t>(4, batch - b0);
+  // 5-8 vectors of 4-byte storage: one pass (matvec_wide_kernel) when the
+  // shapes allow 16-byte chunked streaming; otherwise up to 4 vectors per
+  // pass (8 vectors through the register-only kernel ran at 2.1 TB/s)
+  const bool wide_ok = sizeof(T) == 4 && K % kWideChunk == 0 && lda % 4 == 0 && ldv % 4 == 0 &&
+                       ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(V)) & 15) == 0;
+  for (int64_t b0 = 0; b0 < batch;) {
+    const int64_t left = batch - b0;
+    const int nb = (int)std::min<int64_t>(wide_ok && left > 4 ? kWideNB : 4, left);
     const T* Vb = V + b0 * ldv;
     T* Ob = Out + b0 * ldo;
+    b0 += nb;
+    if constexpr (sizeof(T) == 4) {
+      if (nb > 4) {
+        matvec_wide_kernel<T, MIN><<<(unsigned)ceil_div(M, kWideRows), kWideThreads, 0, st>>>(A, lda, M, K, Vb,
+                                                                                                  ldv, nb,
+                                                                                         Ob, ldo, int_mode, limit,
+                                                                                         flags);
+        BTAS_CUDA_CHECK_LAUNCH();
+        continue;
+      }
+    }
     if (nb == 1) {
       matvec_kernel<T, MIN, 16, 1><<<(unsigned)ceil_div(M, 16), 256, 0, st>>>(A, lda, M, K, Vb, ldv, nb, Ob, ldo,
                                                                             int_mode, limit, flags);
@@ -346,9 +565,6 @@ int matvec_typed(int int_mode, const T* A, int64_t lda, int64_t M, int64_t K, co
                                                                           int_mode, limit, flags);
     } else if (nb <= 4) {
       matvec_kernel<T, MIN, 8, 4><<<(unsigned)ceil_div(M, 8), 256, 0, st>>>(A, lda, M, K, Vb, ldv, nb, Ob, ldo,
-                                                                          int_mode, limit, flags);
-    } else {
-      matvec_kernel<T, MIN, 4, 8><<<(unsigned)ceil_div(M, 4), 256, 0, st>>>(A, lda, M, K, Vb, ldv, nb, Ob, ldo,
                                                                           int_mode, limit, flags);
     }
     BTAS_CUDA_CHECK_LAUNCH();

@@ -172,3 +172,30 @@ def test_host_read_small_results(cuda):
     assert _host_read(t).tobytes() == t.cpu().numpy().tobytes()
     assert _host_read(t[::3]).tobytes() == t[::3].cpu().numpy().tobytes()
     assert _host_read(torch.zeros(0, device="cuda")).shape == (0,)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.int32])
+def test_matvec_wide_saturating(cuda, dtype):
+    """5-8 vectors (one-pass wide kernel) with magnitudes whose sums overflow:
+    the CTA's screen fails and its rows are recomputed with masked candidates."""
+    rng = np.random.default_rng(9)
+    big = 3e38 if dtype == torch.float32 else 2**28 - 1
+    m, k = 70, 512
+    for kind in (MIN, MAX):
+        asym = rng.uniform(-big, big, (m, k))
+        vs = rng.uniform(-big, big, (6, k))
+        if dtype == torch.int32:
+            asym, vs = np.floor(asym), np.floor(vs)
+        else:  # the storage values (f32) are the operands
+            asym, vs = asym.astype(np.float32).astype(np.float64), vs.astype(np.float32).astype(np.float64)
+        asym[rng.random((m, k)) < 0.2] = math.inf
+        asym[:40] = np.clip(asym[:40], -1000, 1000)  # some CTAs pass the screen, some do not
+        a = bt.TropicalMatrix(kind, asym, dtype=dtype)
+        V = bt.TropicalMatrix(kind, vs, dtype=dtype)
+        bt.reset_saturation()
+        out = bm._to_f64(bt.matvec_batched(a, V)).cpu().numpy()
+        assert bt.saturation_seen()
+        for b in range(6):
+            want, sat = ot.matvec(ot.orient(kname(kind), asym), ot.orient(kname(kind), vs[b]), kname(kind),
+                                  STORAGE[dtype], dtype == torch.int32)
+            assert out[b].tobytes() == want.tobytes(), (kind, b)
