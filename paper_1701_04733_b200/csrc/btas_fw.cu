@@ -239,27 +239,51 @@ __global__ void __launch_bounds__(kFwThreads) fw_phase1_kernel(T* __restrict__ D
 // blockIdx.y == 0: row panel (pivot rows x column block blockIdx.x), its own
 //                  row k each round, pivot-column snapshots fixed in smem
 // blockIdx.y == 1: column panel (row block blockIdx.x x pivot columns)
+// The fixed operand of every round (the pivot tile's column / row snapshot,
+// 64 KB, identical for all CTAs) is read through L1 one round ahead instead
+// of being staged in shared memory: a CTA needs only its own history array,
+// so two CTAs share an SM and phase 2's latency-bound rounds overlap.
+template <class T>
+BTAS_D void load_fixed(const T* __restrict__ src, int k, int x0, T (&out)[FwB<T>::R]) {
+  constexpr int b = FwB<T>::b, R = FwB<T>::R;
+  const T* p = src + (int64_t)k * b + x0;
+  if constexpr (R * sizeof(T) % 16 == 0) {
+#pragma unroll
+    for (int q = 0; q < R * (int)sizeof(T) / 16; ++q) {
+      const uint4 u = __ldg(reinterpret_cast<const uint4*>(p) + q);
+      const T* e = reinterpret_cast<const T*>(&u);
+#pragma unroll
+      for (int i = 0; i < 16 / (int)sizeof(T); ++i) out[q * (16 / sizeof(T)) + i] = e[i];
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < R; ++i) out[i] = __ldg(p + i);
+  }
+}
+
 template <class T, int MODE>
-__global__ void __launch_bounds__(kFwThreads) fw_phase2_kernel(T* __restrict__ D, const T* __restrict__ rowsnapP,
-                                                               const T* __restrict__ colsnapT, T* __restrict__ Scol,
-                                                               T* __restrict__ Srow, uint32_t* __restrict__ Scol16,
-                                                               uint32_t* __restrict__ Srow16, FwArgs f) {
+__global__ void __launch_bounds__(kFwThreads, MODE == kChecked ? 1 : 2) fw_phase2_kernel(T* __restrict__ D, const T* __restrict__ rowsnapP,
+                                                                  const T* __restrict__ colsnapT,
+                                                                  T* __restrict__ Scol, T* __restrict__ Srow,
+                                                                  uint32_t* __restrict__ Scol16,
+                                                                  uint32_t* __restrict__ Srow16, FwArgs f) {
   constexpr int b = FwB<T>::b, R = FwB<T>::R;
   const bool row_panel = f.panel_mode == 0 ? blockIdx.y == 0 : f.panel_mode == 1;
   const int blk = row_panel ? (int)blockIdx.x : f.col_blk0 + (int)blockIdx.x;
   if (blk == (int)(f.k0 / b)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* fixed = reinterpret_cast<T*>(smem_raw);  // row panel: colsnapT[k][a]; col panel: rowsnapP[k][c]
-  T* hist = fixed + b * b;                      // row panel: rs[k][c];      col panel: cT[k][a]
+  T* hist = reinterpret_cast<T*>(smem_raw);  // row panel: rs[k][c]; col panel: cT[k][a]
   const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
   const int64_t r0 = row_panel ? f.k0 : (int64_t)blk * b;
   const int64_t c0 = row_panel ? (int64_t)blk * b : f.k0;
-  {
-    const T* src = row_panel ? colsnapT : rowsnapP;
-    for (int e = threadIdx.x; e < b * b; e += blockDim.x) fixed[e] = src[e];
-  }
+  // row panel: fixed = colsnapT[k][a] (this thread's rows a = ty*R..);
+  // col panel: fixed = rowsnapP[k][c] (this thread's cols c = tx*R..)
+  const T* fixedg = row_panel ? colsnapT : rowsnapP;
+  const int fx0 = row_panel ? ty * R : tx * R;
   T v[R][R];
   load_block(D, f, r0, c0, ty, tx, v);
+  T fx[R];
+  load_fixed(fixedg, 0, fx0, fx);
   bool sat = false;
   for (int kb = 0; kb < b; kb += R) {
     const int owner = kb / R;
@@ -277,18 +301,28 @@ __global__ void __launch_bounds__(kFwThreads) fw_phase2_kernel(T* __restrict__ D
           for (int i = 0; i < R; ++i) hist[k * b + ty * R + i] = v[i][kk];
         }
       }
+      T fxn[R];
+      if (k + 1 < b) load_fixed(fixedg, k + 1, fx0, fxn);  // next round's fixed operand, in flight
       __syncthreads();
-      T rowv[R], colv[R];
-      const T* rsrc = row_panel ? hist : fixed;  // [k][c]
-      const T* csrc = row_panel ? fixed : hist;  // [k][a]
+      T own[R];
+      const int ox = row_panel ? tx * R : ty * R;
 #pragma unroll
-      for (int j = 0; j < R; ++j) rowv[j] = rsrc[k * b + tx * R + j];
+      for (int j = 0; j < R; ++j) own[j] = hist[k * b + ox + j];
+      if (row_panel) {
 #pragma unroll
-      for (int i = 0; i < R; ++i) colv[i] = csrc[k * b + ty * R + i];
+        for (int i = 0; i < R; ++i)
 #pragma unroll
-      for (int i = 0; i < R; ++i)
+          for (int j = 0; j < R; ++j) relax<T, MODE>(v[i][j], fx[i], own[j], f.int_mode, f.limit, sat);
+      } else {
 #pragma unroll
-        for (int j = 0; j < R; ++j) relax<T, MODE>(v[i][j], colv[i], rowv[j], f.int_mode, f.limit, sat);
+        for (int i = 0; i < R; ++i)
+#pragma unroll
+          for (int j = 0; j < R; ++j) relax<T, MODE>(v[i][j], own[i], fx[j], f.int_mode, f.limit, sat);
+      }
+      if (k + 1 < b) {
+#pragma unroll
+        for (int i = 0; i < R; ++i) fx[i] = fxn[i];
+      }
     }
   }
   store_block(D, f, r0, c0, ty, tx, v);
@@ -415,7 +449,7 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
   f.ctrl = ctrl;
 
   const size_t smem1 = 2 * (size_t)b * b * sizeof(T);
-  const size_t smem2 = 2 * (size_t)b * b * sizeof(T);
+  const size_t smem2 = (size_t)b * b * sizeof(T);  // phase 2: the history array only
   static bool configured = false;
   if (!configured) {
     if (cudaFuncSetAttribute(fw_phase1_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -622,11 +656,12 @@ int fw_dist_stage_typed(int integer_mode, int stage, T* D, int64_t ld, int64_t n
   f.flags = flags;
   f.ctrl = ctrl;
   const size_t smem = 2 * (size_t)b * b * sizeof(T);
+  const size_t smem2 = (size_t)b * b * sizeof(T);
   static bool configured = false;
   if (!configured) {
     if (cudaFuncSetAttribute(fw_phase1_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
             cudaSuccess ||
-        cudaFuncSetAttribute(fw_phase2_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaFuncSetAttribute(fw_phase2_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2) !=
             cudaSuccess) {
       (void)cudaGetLastError();
       return BTAS_ERR_CUDA;
@@ -648,7 +683,8 @@ int fw_dist_stage_typed(int integer_mode, int stage, T* D, int64_t ld, int64_t n
       fw_phase1_kernel<T, MODE><<<1, kFwThreads, smem, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
       if (nblk > 1) {
         f.panel_mode = 1;
-        fw_phase2_kernel<T, MODE><<<dim3(nblk, 1), kFwThreads, smem, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
+        fw_phase2_kernel<T, MODE><<<dim3(nblk, 1), kFwThreads, smem2, st>>>(D, rsp, csp, scol, srow, scol16, srow16,
+                                                                            f);
       }
       break;
     }
@@ -657,7 +693,7 @@ int fw_dist_stage_typed(int integer_mode, int stage, T* D, int64_t ld, int64_t n
       f.panel_mode = 2;
       f.col_blk0 = (int)(slab_r0 / b);
       const int nsb = (int)ceil_div(slab_rows, b);
-      fw_phase2_kernel<T, MODE><<<dim3(nsb, 1), kFwThreads, smem, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
+      fw_phase2_kernel<T, MODE><<<dim3(nsb, 1), kFwThreads, smem2, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
       break;
     }
     case BTAS_FW_STAGE_UPDATE: {
