@@ -278,7 +278,8 @@ int btas_graph_draw(const btas_pcg64* rng, int64_t n, int weights_mode, uint64_t
                     double scale, int64_t edges, uint64_t unit0, uint64_t units, void* draws,
                     void* workspace, size_t workspace_bytes, int64_t* dev_accepted, btas_stream_t stream);
 /* stage 3 (graph_to_matrix): dense n x n min-plus storage of dtype into D (leading dim ld);
- * reuses stage 1's counts in the workspace; stats as btas_ingest reports them. */
+ * reuses stage 1's presence record and counts in the workspace (rng and p_threshold
+ * must be stage 1's); stats as btas_ingest reports them. */
 int btas_graph_fill(int dtype, const btas_pcg64* rng, int64_t n, uint64_t p_threshold, int weights_mode,
                     uint64_t range, int64_t low, const void* draws, void* D, int64_t ld,
                     const void* workspace, size_t workspace_bytes, btas_stats* stats_dev,

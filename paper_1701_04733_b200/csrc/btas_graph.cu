@@ -17,9 +17,10 @@
 //             draws with numpy's exact rejection rule (32-bit buffered words
 //             lo-then-hi, or 64-bit words), or uniform doubles; accepted draws
 //             are compacted in stream order into a dense array
-//   fill      regenerate presence, rank each present pair, write the dense
-//             row-major matrix (diagonal 0, absent +inf) through the same
-//             float64 -> storage conversion and statistics as btas_ingest
+//   fill      read stage 1's presence ballots (one word per 32 pairs), rank
+//             each present pair, write the dense row-major matrix (diagonal
+//             0, absent +inf) through the same float64 -> storage conversion
+//             and statistics as btas_ingest
 #include <algorithm>
 #include <type_traits>
 
@@ -125,20 +126,25 @@ BTAS_D int64_t warp_base(const int32_t* warp_cnt, const int64_t* cta_base) {
 
 // ------------------------------------------------------------------ presence
 __global__ void __launch_bounds__(kGenThreads) presence_kernel(const __grid_constant__ PcgJumps J, uint64_t pairs,
-                                                               uint64_t thr, int32_t* warp_cnt, int32_t* cta_cnt) {
-  const uint64_t q0 = (uint64_t)blockIdx.x * kCtaUnits + (uint64_t)(threadIdx.x >> 5) * kWarpUnits + (threadIdx.x & 31);
+                                                               uint64_t thr, int32_t* warp_cnt, int32_t* cta_cnt,
+                                                               uint32_t* __restrict__ bits) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t w0 = (uint64_t)blockIdx.x * kCtaUnits + (uint64_t)(threadIdx.x >> 5) * kWarpUnits;
+  const uint64_t q0 = w0 + lane;
   int cnt = 0;
-  if (q0 - (threadIdx.x & 31) < pairs) {  // warp-uniform
+  if (w0 < pairs) {  // warp-uniform
     U128 s = state_at(J, q0);
+    uint32_t mine = 0;  // lane i keeps the ballot word of iteration i (mod 32)
 #pragma unroll 4
     for (int it = 0; it < kGenIters; ++it) {
       const uint64_t q = q0 + 32ull * it;
-      if (q < pairs && (xslrr(s) >> 11) < thr) cnt++;
+      const unsigned b = __ballot_sync(0xffffffffu, q < pairs && (xslrr(s) >> 11) < thr);
+      cnt += __popc(b);
+      if ((it & 31) == lane) mine = b;
+      if ((it & 31) == 31) bits[w0 / 32 + (it & ~31) + lane] = mine;  // 32 words, coalesced
       s = stride32(J, s);
     }
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
   store_counts(cnt, warp_cnt, cta_cnt);
 }
 
@@ -259,10 +265,10 @@ __global__ void __launch_bounds__(kGenThreads) draw_kernel(const __grid_constant
 
 // ------------------------------------------------------------------ fill
 template <class D>
-__global__ void __launch_bounds__(kGenThreads) fill_kernel(const __grid_constant__ PcgJumps J, int64_t n,
-                                                           uint64_t thr, int wmode, bool wide, int64_t low,
+__global__ void __launch_bounds__(kGenThreads) fill_kernel(int64_t n, int wmode, bool wide, int64_t low,
                                                            const void* __restrict__ draws, D* __restrict__ out,
-                                                           int64_t ld, const int32_t* __restrict__ warp_cnt,
+                                                           int64_t ld, const uint32_t* __restrict__ bits,
+                                                           const int32_t* __restrict__ warp_cnt,
                                                            const int64_t* __restrict__ cta_base, int64_t ctas,
                                                            btas_stats* stats) {
   using A = typename std::conditional<Traits<D>::dtype == BTAS_F32, float, double>::type;
@@ -272,20 +278,21 @@ __global__ void __launch_bounds__(kGenThreads) fill_kernel(const __grid_constant
   const int64_t gtid = (int64_t)blockIdx.x * kGenThreads + threadIdx.x;
   if (gtid < n) out[gtid * ld + gtid] = ingest_one<double, D, A>(0.0, inf, st);  // graph_to_matrix diagonal
   const uint64_t pairs = (uint64_t)n * (uint64_t)(n - 1);
-  const uint64_t q0 = (uint64_t)blockIdx.x * kCtaUnits + (uint64_t)(threadIdx.x >> 5) * kWarpUnits + lane;
-  if (blockIdx.x < ctas && q0 - lane < pairs) {
+  const uint64_t w0 = (uint64_t)blockIdx.x * kCtaUnits + (uint64_t)(threadIdx.x >> 5) * kWarpUnits;
+  if (blockIdx.x < ctas && w0 < pairs) {
     int64_t rank = warp_base(warp_cnt, cta_base);
     const int64_t row_len = n - 1;
+    const uint64_t q0 = w0 + lane;
     int64_t row = (int64_t)(q0 / (uint64_t)row_len);
     int64_t j = (int64_t)(q0 - (uint64_t)row * row_len);
-    U128 s = state_at(J, q0);
-#pragma unroll 2
+    const uint32_t* wb = bits + w0 / 32;
+    uint32_t mine = 0;
     for (int it = 0; it < kGenIters; ++it) {
+      if ((it & 31) == 0) mine = wb[it + lane];  // 32 presence words per coalesced load
+      const unsigned b = __shfl_sync(0xffffffffu, mine, it & 31);
       const uint64_t q = q0 + 32ull * it;
-      const bool valid = q < pairs;
-      const bool present = valid && (xslrr(s) >> 11) < thr;
-      const unsigned b = __ballot_sync(0xffffffffu, present);
-      if (valid) {
+      if (q < pairs) {
+        const bool present = (b >> lane) & 1u;
         double w = INFINITY;
         if (present) {
           const int64_t m = rank + warp_excl(b);
@@ -302,7 +309,6 @@ __global__ void __launch_bounds__(kGenThreads) fill_kernel(const __grid_constant
         out[row * ld + j + (j >= row ? 1 : 0)] = ingest_one<double, D, A>(w, inf, st);
       }
       rank += __popc(b);
-      s = stride32(J, s);
       j += 32;
       while (j >= row_len) {
         j -= row_len;
@@ -415,6 +421,7 @@ int edges_typed(int64_t n, const int64_t* src, const int64_t* dst, const double*
 
 // ------------------------------------------------------------------ host
 struct GraphWs {
+  uint32_t* bits;  // presence ballots of stage 1, one word per 32 pairs
   int32_t *p_warp, *p_cta, *d_warp, *d_cta;
   int64_t *p_base, *d_base;
   int64_t p_ctas, d_ctas;
@@ -433,6 +440,7 @@ GraphWs graph_ws(int64_t n, void* base) {
     off += (size_t)round_up((int64_t)bytes, 256);
     return p;
   };
+  w.bits = (uint32_t*)take(sizeof(uint32_t) * std::max<int64_t>(1, w.p_ctas) * (kCtaUnits / 32));
   w.p_warp = (int32_t*)take(sizeof(int32_t) * std::max<int64_t>(1, w.p_ctas) * kGenWarps);
   w.p_cta = (int32_t*)take(sizeof(int32_t) * std::max<int64_t>(1, w.p_ctas));
   w.p_base = (int64_t*)take(sizeof(int64_t) * std::max<int64_t>(1, w.p_ctas));
@@ -464,7 +472,7 @@ extern "C" int btas_graph_presence(const btas_pcg64* rng, int64_t n, uint64_t p_
   const uint64_t pairs = (uint64_t)n * (uint64_t)(n - 1);
   const PcgJumps J = make_jumps(*rng);
   if (w.p_ctas > 0) {
-    presence_kernel<<<(unsigned)w.p_ctas, kGenThreads, 0, st>>>(J, pairs, p_threshold, w.p_warp, w.p_cta);
+    presence_kernel<<<(unsigned)w.p_ctas, kGenThreads, 0, st>>>(J, pairs, p_threshold, w.p_warp, w.p_cta, w.bits);
     BTAS_CUDA_CHECK_LAUNCH();
   }
   scan_kernel<<<1, kScanThreads, 0, st>>>(w.p_cta, w.p_ctas, w.p_base, nullptr, dev_edges);
@@ -546,25 +554,24 @@ extern "C" int btas_graph_fill(int dtype, const btas_pcg64* rng, int64_t n, uint
   const GraphWs w = graph_ws(n, const_cast<void*>(workspace));
   if (workspace_bytes < w.bytes) return BTAS_ERR_WORKSPACE;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const PcgJumps J = make_jumps(*rng);
   const bool wide = weights_mode == BTAS_WEIGHTS_BOUNDED && range > 0xFFFFFFFFull;
   const int64_t grid = std::max<int64_t>(w.p_ctas, ceil_div(n, kGenThreads));
   if (grid > 0x7FFFFFFF) return BTAS_ERR_UNSUPPORTED;
   switch (dtype) {
     case BTAS_F32:
-      fill_kernel<float><<<(unsigned)grid, kGenThreads, 0, st>>>(J, n, p_threshold, weights_mode, wide, low, draws,
-                                                                  static_cast<float*>(D), ld, w.p_warp, w.p_base,
-                                                                  w.p_ctas, stats_dev);
+      fill_kernel<float><<<(unsigned)grid, kGenThreads, 0, st>>>(n, weights_mode, wide, low, draws,
+                                                              static_cast<float*>(D), ld, w.bits, w.p_warp,
+                                                              w.p_base, w.p_ctas, stats_dev);
       break;
     case BTAS_I32:
-      fill_kernel<int32_t><<<(unsigned)grid, kGenThreads, 0, st>>>(J, n, p_threshold, weights_mode, wide, low,
-                                                                    draws, static_cast<int32_t*>(D), ld, w.p_warp,
-                                                                    w.p_base, w.p_ctas, stats_dev);
+      fill_kernel<int32_t><<<(unsigned)grid, kGenThreads, 0, st>>>(n, weights_mode, wide, low, draws,
+                                                              static_cast<int32_t*>(D), ld, w.bits, w.p_warp,
+                                                              w.p_base, w.p_ctas, stats_dev);
       break;
     case BTAS_F64:
-      fill_kernel<double><<<(unsigned)grid, kGenThreads, 0, st>>>(J, n, p_threshold, weights_mode, wide, low, draws,
-                                                                   static_cast<double*>(D), ld, w.p_warp, w.p_base,
-                                                                   w.p_ctas, stats_dev);
+      fill_kernel<double><<<(unsigned)grid, kGenThreads, 0, st>>>(n, weights_mode, wide, low, draws,
+                                                              static_cast<double*>(D), ld, w.bits, w.p_warp,
+                                                              w.p_base, w.p_ctas, stats_dev);
       break;
     default:
       return BTAS_ERR_INVALID;
