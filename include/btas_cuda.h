@@ -61,7 +61,8 @@ enum {
   BTAS_PATH_S16X2 = 1,   /* integer operands with |x| < 2^12: VIADDMNMX.S16x2, 2 pairs/instr */
   BTAS_PATH_CHECKED = 2, /* per-candidate overflow masking (the reference's masked tile) */
   BTAS_PATH_FAST64 = 3,  /* f64 DADD + min */
-  BTAS_PATH_EMPTY = 4    /* no work (an operand has no rows/cols) */
+  BTAS_PATH_EMPTY = 4,   /* no work (an operand has no rows/cols) */
+  BTAS_PATH_I32F64 = 5   /* f64 integer operands whose sums stay inside the int32 domain: VIADDMNMX */
 };
 
 /* status codes */

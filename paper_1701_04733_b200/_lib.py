@@ -25,13 +25,14 @@ I32_INF = 0x3FFFFFFF
 I32_LIMIT = 1 << 28
 FLAG_CHANGED, FLAG_DIAG_NEG, FLAG_SATURATED, FLAG_PATH = 0, 1, 2, 3
 NUM_FLAGS = 8
-PATH_FAST32, PATH_S16X2, PATH_CHECKED, PATH_FAST64, PATH_EMPTY = 0, 1, 2, 3, 4
+PATH_FAST32, PATH_S16X2, PATH_CHECKED, PATH_FAST64, PATH_EMPTY, PATH_I32F64 = 0, 1, 2, 3, 4, 5
 PATH_NAMES = {
     PATH_FAST32: "fast32",
     PATH_S16X2: "s16x2",
     PATH_CHECKED: "checked",
     PATH_FAST64: "fast64",
     PATH_EMPTY: "empty",
+    PATH_I32F64: "i32f64",
 }
 OK, ERR_INVALID, ERR_CUDA, ERR_WORKSPACE, ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 APSP_SMALL_MAX_N = 1024

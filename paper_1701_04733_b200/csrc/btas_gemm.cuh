@@ -120,6 +120,35 @@ struct MixI32 {
   }
 };
 
+// float64 storage, integer operands whose every finite sum stays inside the
+// int32 domain (|a| + |b| < 2^28, decided by the exact screen): the packed
+// operands are int32 (Inf -> +/-(2^30-1)) and the add-min is VIADDMNMX, 5x the
+// DADD+min rate.  Sums are exact integers in both representations, so the
+// float64 result is the same bytes.
+template <bool MIN>
+struct MixI32F64 {
+  using E = int32_t;
+  using Acc = int32_t;
+  using Out = double;
+  static constexpr int GM = 4, GN = 4, KP = 16, STAGES = 4;
+  static constexpr int path = BTAS_PATH_I32F64;
+  static constexpr bool kChecked = false;
+  BTAS_D static Acc init() { return MIN ? kI32Inf : -kI32Inf; }
+  BTAS_D static void step(Acc& c, E a0, E a1, E b0, E b1, bool&, const GemmArgs&) {
+    if (MIN) {
+      c = __viaddmin_s32(a0, b0, c);
+      c = __viaddmin_s32(a1, b1, c);
+    } else {
+      c = __viaddmax_s32(a0, b0, c);
+      c = __viaddmax_s32(a1, b1, c);
+    }
+  }
+  BTAS_D static Out finish(Acc c, const GemmArgs&) {
+    if (MIN) return c >= kI32Limit ? INFINITY : (double)c;
+    return c <= -kI32Limit ? -INFINITY : (double)c;
+  }
+};
+
 template <bool MIN>
 struct MixF64 {
   using E = double;

@@ -5,6 +5,7 @@
 #pragma once
 
 #include <algorithm>
+#include <type_traits>
 
 #include "btas_gemm.cuh"
 
@@ -231,6 +232,8 @@ __global__ void screen_kernel(const unsigned long long* __restrict__ extA, const
       path = BTAS_PATH_CHECKED;
     } else if (integer_mode && amax < (double)kS16Limit && bmax < (double)kS16Limit) {
       path = BTAS_PATH_S16X2;
+    } else if (Traits<T>::dtype == BTAS_F64 && integer_mode && amax + bmax < (double)kI32Limit) {
+      path = BTAS_PATH_I32F64;  // no sum reaches 2^28 (< the 2^53 limit): nothing saturates
     } else {
       path = Traits<T>::dtype == BTAS_F64 ? BTAS_PATH_FAST64 : BTAS_PATH_FAST32;
     }
@@ -254,7 +257,11 @@ BTAS_D E load_virtual(const T* __restrict__ X, int64_t ld, int64_t rows, int64_t
                       bool c_is_k) {
   // c_is_k: virtual column index c is along k (A operand, row r); otherwise
   // the virtual row index r is along k (B operand, column c).
-  if constexpr (!S16) {
+  if constexpr (!S16 && std::is_integral<E>::value && !std::is_integral<T>::value) {
+    // float64 integer operands packed as int32 (BTAS_PATH_I32F64)
+    const T x = (r < rows && c < cols) ? X[r * ld + c] : Traits<T>::eps(MIN);
+    return isfinite(x) ? (E)x : (MIN ? (E)kI32Inf : (E)-kI32Inf);
+  } else if constexpr (!S16) {
     if (r < rows && c < cols) return (E)X[r * ld + c];
     return (E)Traits<T>::eps(MIN);
   } else {
@@ -376,6 +383,30 @@ int gemm_typed(int integer_mode, const T* A, int64_t lda, const T* B, int64_t ld
     g.n_peers = n_peers;
     for (int q = 0; q < n_peers && q < kMaxPeers; ++q) g.peer_C[q] = peers[q];
   }
+  GemmArgs g32{};  // float64 integer operands through the int32 kernel
+  if constexpr (kIsF64) {
+    if (int_mode) {
+      const int64_t Kp2 = round_up(K, 2 * kKP) / 2;
+      const int64_t Mp = round_up(M, 128), Np = round_up(N, 128);
+      int32_t* Ap = reinterpret_cast<int32_t*>(ws + L.packA);
+      int32_t* Bp = reinterpret_cast<int32_t*>(ws + L.packB);
+      dim3 ga((unsigned)ceil_div(2 * Kp2, 64), (unsigned)ceil_div(Mp, 32));
+      pack_a_kernel<T, int32_t, false, MIN, 128><<<ga, 256, 0, st>>>(A, lda, M, K, 2 * Kp2, Kp2, Ap, ctrl,
+                                                                      BTAS_PATH_I32F64, BTAS_PATH_I32F64);
+      const int64_t tb = Kp2 * Np;
+      pack_b_kernel<T, int32_t, false, MIN, 128><<<(unsigned)std::min<int64_t>(ceil_div(tb, 256), 65535), 256, 0,
+                                                    st>>>(B, ldb, K, N, Np, Kp2, Bp, ctrl, BTAS_PATH_I32F64,
+                                                          BTAS_PATH_I32F64);
+      BTAS_CUDA_CHECK_LAUNCH();
+      g32 = g;
+      g32.Ap = Ap;
+      g32.Bp = Bp;
+      g32.Kp2 = Kp2;
+      g32.mblocks = (int)(Mp / 128);
+      g32.nblocks = (int)(Np / 128);
+      g32.gate_value = BTAS_PATH_I32F64;
+    }
+  }
   GemmArgs g16{};  // int16x2 path (integer operands with |x| < 2^12)
   const int bn16 = 32 * s16_gn();
   if (int_mode) {
@@ -422,6 +453,10 @@ int gemm_typed(int integer_mode, const T* A, int64_t lda, const T* B, int64_t ld
   if (int_mode) {
     rc = launch_tropical_gemm<MixS16<MIN, T, 4>, MIN>(g16, st);
     if (rc) return rc;
+    if constexpr (kIsF64) {
+      rc = launch_tropical_gemm<MixI32F64<MIN>, MIN>(g32, st);
+      if (rc) return rc;
+    }
   }
   timing_end(st, t0);
   return BTAS_OK;

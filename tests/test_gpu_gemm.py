@@ -65,7 +65,21 @@ def test_kernel_path_selection(cuda):
         assert _paths(a, b, True)[1] == {"s16x2"}
         a = bt.TropicalMatrix(MIN, wide, dtype=dt)
         b = bt.TropicalMatrix(MIN, wide.T.copy(), dtype=dt)
-        assert _paths(a, b, True)[1] == ({"fast64"} if dt == torch.float64 else {"fast32"})
+        assert _paths(a, b, True)[1] == ({"i32f64"} if dt == torch.float64 else {"fast32"})
+    # float64 integer operands beyond the int32 domain keep the DADD path
+    huge = rand_sym(rng, 40, 50, -2**40, 2**40)
+    a = bt.TropicalMatrix(MIN, huge, dtype=torch.float64)
+    b = bt.TropicalMatrix(MIN, huge.T.copy(), dtype=torch.float64)
+    assert _paths(a, b, True)[1] == {"fast64"}
+    for v, path in ((2.0**27 - 1, "i32f64"), (2.0**27, "fast64")):  # sums 2^28 - 2 / 2^28
+        for kind in (MIN, MAX):
+            sym = np.full((3, 3), v)
+            sym[0, 1] = math.inf
+            a = bt.TropicalMatrix(kind, sym, dtype=torch.float64)
+            out, paths = _paths(a, a, True, kind)
+            assert paths == {path}
+            want, _ = ot.matmul(ot.orient(kname(kind), sym), ot.orient(kname(kind), sym), kname(kind), "f64", True)
+            assert bm._to_f64(out).cpu().numpy().tobytes() == want.tobytes()
     for dt in (torch.float32, torch.float64):
         a = bt.TropicalMatrix(MIN, real, dtype=dt)
         b = bt.TropicalMatrix(MIN, real.T.copy(), dtype=dt)
