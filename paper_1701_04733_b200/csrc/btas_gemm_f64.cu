@@ -1,14 +1,14 @@
-// btas_gemm driver instantiated for double storage (see btas_gemm_impl.cuh).
+// btas_gemm driver (min-plus half) instantiated for double storage (see btas_gemm_impl.cuh).
 #include "btas_gemm_impl.cuh"
 
 namespace btas {
 
 BTAS_GEMM_DRIVER_DECL(double, gemm_f64) {
+  if (!min_plus) return gemm_f64_max(integer_mode, A, lda, B, ldb, Z, ldz, C, ldc, M, N, K, Cprev, ldcp, flags, ws,
+                                     peers, n_peers, st);
   const gemm_impl::WsLayout L = gemm_impl::ws_layout(Traits<double>::dtype, M, N, K);
-  return min_plus ? gemm_impl::gemm_typed<double, true>(integer_mode, A, lda, B, ldb, Z, ldz, C, ldc, M, N, K, Cprev,
-                                                      ldcp, flags, ws, L, peers, n_peers, st)
-                  : gemm_impl::gemm_typed<double, false>(integer_mode, A, lda, B, ldb, Z, ldz, C, ldc, M, N, K, Cprev,
-                                                       ldcp, flags, ws, L, peers, n_peers, st);
+  return gemm_impl::gemm_typed<double, true>(integer_mode, A, lda, B, ldb, Z, ldz, C, ldc, M, N, K, Cprev, ldcp, flags, ws,
+                                         L, peers, n_peers, st);
 }
 
 }  // namespace btas

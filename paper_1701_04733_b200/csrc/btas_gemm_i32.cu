@@ -1,14 +1,14 @@
-// btas_gemm driver instantiated for int32_t storage (see btas_gemm_impl.cuh).
+// btas_gemm driver (min-plus half) instantiated for int32_t storage (see btas_gemm_impl.cuh).
 #include "btas_gemm_impl.cuh"
 
 namespace btas {
 
 BTAS_GEMM_DRIVER_DECL(int32_t, gemm_i32) {
+  if (!min_plus) return gemm_i32_max(integer_mode, A, lda, B, ldb, Z, ldz, C, ldc, M, N, K, Cprev, ldcp, flags, ws,
+                                     peers, n_peers, st);
   const gemm_impl::WsLayout L = gemm_impl::ws_layout(Traits<int32_t>::dtype, M, N, K);
-  return min_plus ? gemm_impl::gemm_typed<int32_t, true>(integer_mode, A, lda, B, ldb, Z, ldz, C, ldc, M, N, K, Cprev,
-                                                      ldcp, flags, ws, L, peers, n_peers, st)
-                  : gemm_impl::gemm_typed<int32_t, false>(integer_mode, A, lda, B, ldb, Z, ldz, C, ldc, M, N, K, Cprev,
-                                                       ldcp, flags, ws, L, peers, n_peers, st);
+  return gemm_impl::gemm_typed<int32_t, true>(integer_mode, A, lda, B, ldb, Z, ldz, C, ldc, M, N, K, Cprev, ldcp, flags, ws,
+                                         L, peers, n_peers, st);
 }
 
 }  // namespace btas

@@ -474,6 +474,15 @@ int gemm_typed(int integer_mode, const T* A, int64_t lda, const T* B, int64_t ld
 BTAS_GEMM_DRIVER_DECL(float, gemm_f32);
 BTAS_GEMM_DRIVER_DECL(int32_t, gemm_i32);
 BTAS_GEMM_DRIVER_DECL(double, gemm_f64);
+// the max-plus halves live in their own translation units (btas_gemm_*_max.cu)
+// so the six kernel families compile in parallel
+#define BTAS_GEMM_HALF_DECL(T, NAME)                                                                          \
+  int NAME(int integer_mode, const T* A, int64_t lda, const T* B, int64_t ldb, const T* Z, int64_t ldz, T* C,    \
+           int64_t ldc, int64_t M, int64_t N, int64_t K, const T* Cprev, int64_t ldcp, int32_t* flags,         \
+           unsigned char* ws, void* const* peers, int n_peers, cudaStream_t st)
+BTAS_GEMM_HALF_DECL(float, gemm_f32_max);
+BTAS_GEMM_HALF_DECL(int32_t, gemm_i32_max);
+BTAS_GEMM_HALF_DECL(double, gemm_f64_max);
 size_t gemm_ws_total(int dtype, int64_t M, int64_t N, int64_t K);
 
 }  // namespace btas
