@@ -493,6 +493,7 @@ def variants(n, dev, rank):
         "f32_integer_valued": (torch.float32, False, 1000),
         "f32_real_valued": (torch.float32, True, 1000),
         "i32_wide_range": (torch.int32, False, 10**6),
+        "f64_integer_wide_range": (torch.float64, False, 10**6),  # the reference's default dtype
     }
     for name, (dtype, real, rng) in cases.items():
         g = torch.Generator(device=dev)
@@ -523,7 +524,7 @@ def variants(n, dev, rank):
         kms, kc = _lib.gemm_timing_read()
         _lib.gemm_timing(False)
         ms = s.elapsed_time(e) / 3
-        mix = {"s16x2": 2}.get(path, 1 if dtype == torch.int32 else 0)
+        mix = {"s16x2": 2, "i32f64": 1}.get(path, 1 if dtype == torch.int32 else 0)
         probe = _lib.probe_ceiling(mix)
         nsm = torch.cuda.get_device_properties(dev).multi_processor_count
         peak = probe["pairs_per_clk_sm"] * nsm * probe["sm_mhz"] * 1e6 / 1e12
