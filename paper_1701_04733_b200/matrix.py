@@ -133,19 +133,23 @@ def _ptr(t: torch.Tensor) -> int:
 
 
 class _Workspace:
-    """Per-device growable scratch buffer for the C-ABI calls (never freed
-    mid-stream: the caching allocator keeps the bytes stream-ordered)."""
+    """Growable scratch buffer for the C-ABI calls, one per (device, stream):
+    calls on different streams may run concurrently, calls on one stream are
+    ordered, so a per-stream buffer is never shared by two running kernels.
+    A replaced buffer goes back to the caching allocator, which only reuses it
+    on the same stream (stream-ordered)."""
 
     def __init__(self):
-        self._bufs: "dict[int, torch.Tensor]" = {}
+        self._bufs: "dict[tuple[int, int], torch.Tensor]" = {}
         self._lock = threading.Lock()
 
     def get(self, device: torch.device, nbytes: int) -> torch.Tensor:
+        key = (device.index, torch.cuda.current_stream(device).cuda_stream)
         with self._lock:
-            buf = self._bufs.get(device.index)
+            buf = self._bufs.get(key)
             if buf is None or buf.numel() < nbytes:
                 buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
-                self._bufs[device.index] = buf
+                self._bufs[key] = buf
             return buf
 
 
