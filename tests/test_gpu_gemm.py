@@ -260,3 +260,29 @@ def test_gemm_kernel_timing_hook(cuda):
     finally:
         _lib.gemm_timing(False)
     assert count == 2 and ms > 0
+
+
+def test_f64_integer_path_epilogues(cuda, monkeypatch):
+    """BTAS_PATH_I32F64 through every epilogue: plain, accumulate_into, the
+    fixpoint compare of the squaring loop, and max-plus."""
+    rng = np.random.default_rng(44)
+    for kind in (MIN, MAX):
+        xs, ys, zs = (rand_sym(rng, 150, 190, -10**6, 10**6), rand_sym(rng, 190, 130, -10**6, 10**6),
+                      rand_sym(rng, 150, 130, -10**6, 10**6))
+        x, y, z = (bt.TropicalMatrix(kind, m, dtype=torch.float64) for m in (xs, ys, zs))
+        out, paths = _paths(x, y, True, kind)
+        assert paths == {"i32f64"}
+        k = kname(kind)
+        want, _ = ot.matmul(ot.orient(k, xs), ot.orient(k, ys), k, "f64", True)
+        assert bt.matmul(x, y).to_numpy().tobytes() == want.tobytes()
+        want_acc = ot.ew_add(want, ot.orient(k, zs), k)
+        assert bt.matmul(x, y, accumulate_into=z).to_numpy().tobytes() == want_acc.tobytes()
+    # squaring loop (Cprev compare) on the general path, float64 wide weights
+    monkeypatch.setenv("BTAS_APSP_SMALL_MAX_N", "0")
+    from paper_1701_04733_b200.graphs import random_graph_matrix
+
+    adj = random_graph_matrix(300, 0.05, (1, 10**5), 91, dtype=torch.float64)
+    got = bt.apsp_by_squaring(adj)
+    want, neg, mults, _ = ot.apsp_by_squaring(adj.to_numpy(), "f64", True)
+    assert (got.multiplications_performed, got.negative_cycle) == (mults, neg)
+    assert got.distances.dist.to_numpy().tobytes() == want.tobytes()
