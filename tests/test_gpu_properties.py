@@ -137,3 +137,34 @@ def test_strict_verifier_rejects_fixpoints_below_the_closure(cuda):
     assert bt.verify_apsp_strict(three, good)
     msg = bt.find_apsp_violation_strict(three, bt.DistanceMatrix.from_matrix(zeros))
     assert "closure" in msg
+
+
+@settings(max_examples=60, deadline=None)
+@given(st.integers(1, 300), st.sampled_from([0.0, 0.01, 0.3, 0.5, 1.0]),
+       st.sampled_from([(1, 100), (0, 0), (-5, 7), (0, 2**31), (-(2**33), 2**33), (0.25, 9.5), (3.5, 3.5)]),
+       st.integers(0, 2**63 - 1), st.sampled_from([torch.float64, torch.float32]))
+def test_instance_generator_matches_host(cuda, n, p, wr, seed, dtype):
+    """random_graph_matrix (device PCG64 stream) == the host restatement over
+    random sizes, probabilities, weight families and seeds."""
+    from paper_1701_04733_b200.graphs import random_graph_matrix, random_graph_matrix_host
+
+    got = random_graph_matrix(n, p, wr, seed, dtype=dtype)
+    want = random_graph_matrix_host(n, p, wr, seed, dtype=dtype)
+    assert torch.equal(got.data.view(torch.uint8) if dtype == torch.float32 else got.data.view(torch.int64),
+                       want.data.view(torch.uint8) if dtype == torch.float32 else want.data.view(torch.int64))
+    assert got.integer == want.integer
+
+
+@settings(max_examples=60, deadline=None)
+@given(st.integers(1, 40), st.integers(0, 400), st.integers(0, 2**31 - 1), st.sampled_from(DTYPES))
+def test_edge_list_matches_oracle(cuda, n, m, seed, dtype):
+    from oracle.graphs import graph_to_matrix_edges
+    from paper_1701_04733_b200.graphs import edges_to_matrix
+
+    rng = np.random.default_rng(seed)
+    src, dst = rng.integers(0, n, m), rng.integers(0, n, m)
+    w = rng.integers(-20, 60, m).astype(np.float64)
+    w[rng.random(m) < 0.1] = -0.0
+    got = edges_to_matrix(n, src, dst, w, dtype=dtype)
+    want = graph_to_matrix_edges(n, src, dst, w)
+    assert got.to_numpy().tobytes() == want.tobytes()
