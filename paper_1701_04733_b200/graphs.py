@@ -234,8 +234,12 @@ def edges_to_matrix(n: int, src, dst, weight, *, dtype: "torch.dtype | None" = N
 
 
 def graph_to_matrix(g, *, dtype: "torch.dtype | None" = None, device=None) -> TropicalMatrix:
-    """graph_io.graph_to_matrix (graph_io.py:158-165) for a reference ``Graph``
-    (anything with ``.n`` and ``.edges`` = ((src, dst, weight), ...))."""
+    """graph_io.graph_to_matrix (graph_io.py:158-165) for a ``Graph`` (ours or
+    the reference's: anything with ``.n`` and ``.edges`` = ((src, dst,
+    weight), ...)).  A ``random_graph`` recipe is generated on the GPU."""
+    if isinstance(g, RandomGraph):
+        n, p, wr, seed = g.recipe
+        return random_graph_matrix(n, p, wr, seed, dtype=dtype, device=device)
     edges = tuple(g.edges)
     if edges:
         arr = np.asarray([(float(a), float(b), float(w)) for a, b, w in edges], dtype=np.float64)
@@ -244,3 +248,104 @@ def graph_to_matrix(g, *, dtype: "torch.dtype | None" = None, device=None) -> Tr
         src = dst = np.zeros(0, dtype=np.int64)
         w = np.zeros(0, dtype=np.float64)
     return edges_to_matrix(int(g.n), src, dst, w, dtype=dtype, device=device)
+
+
+# ---------------------------------------------------------------------------
+# graph objects (reference graph_io.py:55-87, 168-187, 273-304)
+# ---------------------------------------------------------------------------
+class Graph:
+    """Directed weighted graph with finite weights (reference graph_io.Graph,
+    graph_io.py:55-87): duplicates of one (src, dst) keep the minimum weight,
+    -0.0 becomes 0.0, and the edges are sorted by (src, dst), so equal graphs
+    compare equal.  Immutable."""
+
+    __slots__ = ("n", "_edges")
+
+    def __init__(self, n: int, edges=()):
+        if not isinstance(n, int) or n < 1:
+            raise ValueError(f"vertex count must be a positive integer, got {n!r}")
+        best: "dict[tuple[int, int], float]" = {}
+        for src, dst, weight in edges:
+            if not (0 <= src < n) or not (0 <= dst < n):
+                raise ValueError(f"edge ({src}, {dst}) out of range for n={n}")
+            w = float(weight)
+            if math.isnan(w) or math.isinf(w):
+                raise ValueError(f"edge ({src}, {dst}) weight must be finite, got {w!r}")
+            if w == 0.0:
+                w = 0.0
+            key = (int(src), int(dst))
+            if key not in best or w < best[key]:
+                best[key] = w
+        object.__setattr__(self, "n", n)
+        object.__setattr__(self, "_edges", tuple((a, b, best[(a, b)]) for a, b in sorted(best)))
+
+    def __setattr__(self, name, value):
+        raise AttributeError("Graph is immutable")
+
+    @property
+    def edges(self) -> "tuple[tuple[int, int, float], ...]":
+        return self._edges
+
+    @property
+    def edge_count(self) -> int:
+        return len(self.edges)
+
+    def __eq__(self, other) -> bool:
+        if not hasattr(other, "n") or not hasattr(other, "edges"):
+            return NotImplemented
+        return self.n == other.n and tuple(self.edges) == tuple(other.edges)
+
+    def __hash__(self) -> int:
+        return hash((self.n, self.edges))
+
+    def __repr__(self) -> str:
+        return f"Graph(n={self.n}, edge_count={self.edge_count})"
+
+
+class RandomGraph(Graph):
+    """``random_graph(n, p, weight_range, seed)`` (graph_io.py:273-304) kept as
+    its recipe: ``graph_to_matrix`` builds the matrix on the GPU straight from
+    the PCG64 stream (no edge list at all); ``.edges`` materialises the
+    reference's tuple on first use (host, vectorised)."""
+
+    __slots__ = ("recipe",)
+
+    def __init__(self, n: int, p: float, weight_range, seed: int):
+        p, low, high = _check(n, p, weight_range)
+        object.__setattr__(self, "n", n)
+        object.__setattr__(self, "_edges", None)
+        object.__setattr__(self, "recipe", (n, p, (weight_range[0], weight_range[1]), int(seed)))
+
+    @property
+    def edges(self) -> "tuple[tuple[int, int, float], ...]":
+        if self._edges is None:
+            n, p, wr, seed = self.recipe
+            out = []
+            for r0, block in dense_rows(n, p, wr, seed):
+                rows, cols = np.nonzero(np.isfinite(block))
+                vals = block[rows, cols]
+                keep = (rows + r0) != cols
+                out.extend(zip((rows[keep] + r0).tolist(), cols[keep].tolist(), vals[keep].tolist()))
+            object.__setattr__(self, "_edges", tuple(out))
+        return self._edges
+
+
+def random_graph(n: int, edge_probability: float, weight_range, seed: int) -> RandomGraph:
+    """Seed-deterministic random digraph (reference graph_io.py:273-304); see
+    RandomGraph.  graph_to_matrix(random_graph(...)) is generated on the GPU."""
+    return RandomGraph(n, edge_probability, weight_range, seed)
+
+
+def matrix_to_graph(m: TropicalMatrix) -> Graph:
+    """Inverse of graph_to_matrix (reference graph_io.py:168-187): finite
+    off-diagonal entries become edges; diagonal entries only when negative."""
+    if m.kind is not SemiringKind.MIN_PLUS:
+        raise ValueError("only min-plus matrices describe graphs")
+    if m.n_rows != m.n_cols:
+        raise ValueError(f"adjacency matrix must be square, got {m.shape}")
+    a = m.to_numpy()
+    keep = np.isfinite(a)
+    diag = np.eye(a.shape[0], dtype=bool)
+    keep &= ~diag | (a < 0.0)
+    rows, cols = np.nonzero(keep)
+    return Graph(m.n_rows, zip(rows.tolist(), cols.tolist(), a[rows, cols].tolist()))

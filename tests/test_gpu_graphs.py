@@ -176,3 +176,19 @@ def test_edge_list_errors_and_graph_objects(cuda):
     s, t = mask.nonzero(as_tuple=True)
     back = edges_to_matrix(300, s, t, d[s, t].double(), dtype=torch.float32)
     assert torch.equal(back.data, d) and back.integer == adj.integer
+
+
+def test_graph_objects_on_the_device(cuda):
+    """graph_to_matrix(random_graph(...)) takes the device generator;
+    matrix_to_graph inverts graph_to_matrix (graph_io.py:168-187)."""
+    import paper_1701_04733_b200 as bt
+
+    for n, p, wr, seed in ((257, 0.3, (1, 100), 5), (40, 0.9, (-3, 8), 6), (1, 0.5, (1, 2), 7)):
+        rg = bt.random_graph(n, p, wr, seed)
+        a = bt.graph_to_matrix(rg, dtype=torch.float64)
+        assert a == random_graph_matrix(n, p, wr, seed, dtype=torch.float64)
+        b = bt.graph_to_matrix(bt.Graph(n, rg.edges), dtype=torch.float64)  # the edge-list route
+        assert a == b
+        assert bt.matrix_to_graph(a) == rg
+    with pytest.raises(ValueError):
+        bt.matrix_to_graph(bt.TropicalMatrix(bt.SemiringKind.MAX_PLUS, [[0.0]]))

@@ -273,3 +273,33 @@ def test_c_oracle_fw_matches_numpy():
         assert n1 == n2
         if not n1:
             assert d1.tobytes() == d2.tobytes()
+
+
+def test_graph_objects_match_reference(golden):
+    """Graph normalisation (graph_io.py:55-87) and random_graph's edge stream
+    (graph_io.py:273-304), host side: re-scattered edge lists reproduce the
+    reference's graph_to_matrix bytes."""
+    from oracle import graphs as og
+    from paper_1701_04733_b200.graphs import Graph, random_graph
+
+    g = golden("edgelist.npz")
+    for case in range(int(g["count"][0])):
+        n = int(g[f"n{case}"][0])
+        gr = Graph(n, zip(g[f"src{case}"].tolist(), g[f"dst{case}"].tolist(), g[f"w{case}"].tolist()))
+        e = np.array(gr.edges, dtype=np.float64).reshape(-1, 3)
+        got = og.graph_to_matrix_edges(n, e[:, 0].astype(np.int64), e[:, 1].astype(np.int64), e[:, 2])
+        assert got.tobytes() == f64(g[f"out{case}"]).tobytes(), case
+        assert list(gr.edges) == sorted(gr.edges) and len({(a, b) for a, b, _ in gr.edges}) == gr.edge_count
+    gen = golden("generator.npz")
+    for i in range(len(gen["n"])):
+        n = int(gen["n"][i])
+        rg = random_graph(n, float(gen["p"][i]), (gen["lo"][i], gen["hi"][i]), int(gen["seed"][i]))
+        e = np.array(rg.edges, dtype=np.float64).reshape(-1, 3)
+        got = og.graph_to_matrix_edges(n, e[:, 0].astype(np.int64), e[:, 1].astype(np.int64), e[:, 2])
+        assert digest(got) == str(gen["digest"][i]), i
+    with pytest.raises(ValueError):
+        Graph(0, ())
+    with pytest.raises(ValueError):
+        Graph(2, [(0, 2, 1.0)])
+    with pytest.raises(ValueError):
+        Graph(2, [(0, 1, math.inf)])
