@@ -116,10 +116,9 @@ struct FwArgs {
 // publish the PRE-round values into the history arrays (which double as the
 // round's operand buffers — written once, so one barrier per round), then
 // every thread relaxes its R x R block.
-template <class T>
+template <class T, int R>
 BTAS_D void load_block(const T* __restrict__ D, const FwArgs& f, int64_t r0, int64_t c0, int ty, int tx,
-                       T (&v)[FwB<T>::R][FwB<T>::R]) {
-  constexpr int R = FwB<T>::R;
+                       T (&v)[R][R]) {
   const T inf = Traits<T>::eps(true);
 #pragma unroll
   for (int i = 0; i < R; ++i) {
@@ -132,10 +131,9 @@ BTAS_D void load_block(const T* __restrict__ D, const FwArgs& f, int64_t r0, int
   }
 }
 
-template <class T>
+template <class T, int R>
 BTAS_D void store_block(T* __restrict__ D, const FwArgs& f, int64_t r0, int64_t c0, int ty, int tx,
-                        const T (&v)[FwB<T>::R][FwB<T>::R]) {
-  constexpr int R = FwB<T>::R;
+                        const T (&v)[R][R]) {
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     const int64_t row = r0 + ty * R + i;
@@ -178,16 +176,20 @@ BTAS_D bool emit_history(const T* __restrict__ h, int64_t rc0, int BLK, const Fw
 
 // ------------------------------------------------------------------ phase 1
 // smem: rs[k][c] (pivot-row history), cT[k][a] (pivot-column history)
+// One CTA of 32 x 32 threads (R1 x R1 values each): the b sequential rounds
+// are barrier-latency-bound, so the pivot tile is spread over 32 warps.
+constexpr int kFw1Threads = 1024;
+
 template <class T, int MODE>
-__global__ void __launch_bounds__(kFwThreads) fw_phase1_kernel(T* __restrict__ D, T* __restrict__ rowsnapP,
-                                                               T* __restrict__ colsnapT, T* __restrict__ Scol,
-                                                               T* __restrict__ Srow, uint32_t* __restrict__ Scol16,
-                                                               uint32_t* __restrict__ Srow16, FwArgs f) {
-  constexpr int b = FwB<T>::b, R = FwB<T>::R;
+__global__ void __launch_bounds__(kFw1Threads) fw_phase1_kernel(T* __restrict__ D, T* __restrict__ rowsnapP,
+                                                                T* __restrict__ colsnapT, T* __restrict__ Scol,
+                                                                T* __restrict__ Srow, uint32_t* __restrict__ Scol16,
+                                                                uint32_t* __restrict__ Srow16, FwArgs f) {
+  constexpr int b = FwB<T>::b, R = b / 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* rs = reinterpret_cast<T*>(smem_raw);
   T* cT = rs + b * b;
-  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+  const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     if (f.group_start) f.ctrl->s16_overflow[0] = 0;
   }
@@ -520,7 +522,7 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
     f.k0 = (int64_t)kb * b;
     f.koff = slot * b;
     f.group_start = slot == 0;
-    fw_phase1_kernel<T, MODE><<<1, kFwThreads, smem1, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
+    fw_phase1_kernel<T, MODE><<<1, kFw1Threads, smem1, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
     if (nblk > 1)
       fw_phase2_kernel<T, MODE><<<dim3(nblk, 2), kFwThreads, smem2, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
     BTAS_CUDA_CHECK_LAUNCH();
@@ -680,7 +682,7 @@ int fw_dist_stage_typed(int integer_mode, int stage, T* D, int64_t ld, int64_t n
     }
     case BTAS_FW_STAGE_PIVOT: {
       if (f.k0 < slab_r0 || f.k0 >= slab_r0 + slab_rows) return BTAS_ERR_INVALID;  // not the owner
-      fw_phase1_kernel<T, MODE><<<1, kFwThreads, smem, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
+      fw_phase1_kernel<T, MODE><<<1, kFw1Threads, smem, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
       if (nblk > 1) {
         f.panel_mode = 1;
         fw_phase2_kernel<T, MODE><<<dim3(nblk, 1), kFwThreads, smem2, st>>>(D, rsp, csp, scol, srow, scol16, srow16,
