@@ -116,30 +116,30 @@ struct FwArgs {
 // publish the PRE-round values into the history arrays (which double as the
 // round's operand buffers — written once, so one barrier per round), then
 // every thread relaxes its R x R block.
-template <class T, int R>
+template <class T, int RI, int RJ>
 BTAS_D void load_block(const T* __restrict__ D, const FwArgs& f, int64_t r0, int64_t c0, int ty, int tx,
-                       T (&v)[R][R]) {
+                       T (&v)[RI][RJ]) {
   const T inf = Traits<T>::eps(true);
 #pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const int64_t row = r0 + ty * R + i;
+  for (int i = 0; i < RI; ++i) {
+    const int64_t row = r0 + ty * RI + i;
 #pragma unroll
-    for (int j = 0; j < R; ++j) {
-      const int64_t col = c0 + tx * R + j;
+    for (int j = 0; j < RJ; ++j) {
+      const int64_t col = c0 + tx * RJ + j;
       v[i][j] = (row < f.slab_r1 && col < f.n) ? D[(row - f.slab_r0) * f.ld + col] : inf;
     }
   }
 }
 
-template <class T, int R>
+template <class T, int RI, int RJ>
 BTAS_D void store_block(T* __restrict__ D, const FwArgs& f, int64_t r0, int64_t c0, int ty, int tx,
-                        const T (&v)[R][R]) {
+                        const T (&v)[RI][RJ]) {
 #pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const int64_t row = r0 + ty * R + i;
+  for (int i = 0; i < RI; ++i) {
+    const int64_t row = r0 + ty * RI + i;
 #pragma unroll
-    for (int j = 0; j < R; ++j) {
-      const int64_t col = c0 + tx * R + j;
+    for (int j = 0; j < RJ; ++j) {
+      const int64_t col = c0 + tx * RJ + j;
       if (row < f.slab_r1 && col < f.n) D[(row - f.slab_r0) * f.ld + col] = v[i][j];
     }
   }
@@ -245,13 +245,13 @@ __global__ void __launch_bounds__(kFw1Threads) fw_phase1_kernel(T* __restrict__ 
 // 64 KB, identical for all CTAs) is read through L1 one round ahead instead
 // of being staged in shared memory: a CTA needs only its own history array,
 // so two CTAs share an SM and phase 2's latency-bound rounds overlap.
-template <class T>
-BTAS_D void load_fixed(const T* __restrict__ src, int k, int x0, T (&out)[FwB<T>::R]) {
-  constexpr int b = FwB<T>::b, R = FwB<T>::R;
+template <class T, int N>
+BTAS_D void load_fixed(const T* __restrict__ src, int k, int x0, T (&out)[N]) {
+  constexpr int b = FwB<T>::b;
   const T* p = src + (int64_t)k * b + x0;
-  if constexpr (R * sizeof(T) % 16 == 0) {
+  if constexpr (N * sizeof(T) % 16 == 0) {
 #pragma unroll
-    for (int q = 0; q < R * (int)sizeof(T) / 16; ++q) {
+    for (int q = 0; q < N * (int)sizeof(T) / 16; ++q) {
       const uint4 u = __ldg(reinterpret_cast<const uint4*>(p) + q);
       const T* e = reinterpret_cast<const T*>(&u);
 #pragma unroll
@@ -259,74 +259,88 @@ BTAS_D void load_fixed(const T* __restrict__ src, int k, int x0, T (&out)[FwB<T>
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < R; ++i) out[i] = __ldg(p + i);
+    for (int i = 0; i < N; ++i) out[i] = __ldg(p + i);
+  }
+}
+
+// phase-2 thread grid: 16 x 32 threads, RI x RJ values each
+constexpr int kFw2Threads = 512;
+template <class T>
+struct Fw2 {
+  static constexpr int RI = FwB<T>::b / 16, RJ = FwB<T>::b / 32;
+};
+
+// the b rounds of one panel tile.  Row panel: each round's own operand is
+// the tile's row k (history, per column), the fixed one the pivot column
+// snapshot (per row).  Column panel: own = the tile's column k (per row),
+// fixed = the pivot row snapshot (per column).
+template <class T, int MODE, bool ROW>
+BTAS_D void phase2_rounds(T (&v)[Fw2<T>::RI][Fw2<T>::RJ], T* hist, const T* __restrict__ fixedg, int ty, int tx,
+                          const FwArgs& f, bool& sat) {
+  constexpr int b = FwB<T>::b, RI = Fw2<T>::RI, RJ = Fw2<T>::RJ;
+  constexpr int NF = ROW ? RI : RJ;  // fixed operand per thread
+  constexpr int NO = ROW ? RJ : RI;  // own operand per thread
+  constexpr int STEP = ROW ? RI : RJ;  // rounds owned by one thread row / column
+  const int fx0 = ROW ? ty * RI : tx * RJ;
+  const int ox0 = ROW ? tx * RJ : ty * RI;
+  T fx[NF];
+  load_fixed(fixedg, 0, fx0, fx);
+  for (int kb = 0; kb < b; kb += STEP) {
+    const int owner = kb / STEP;
+#pragma unroll
+    for (int kk = 0; kk < STEP; ++kk) {
+      const int k = kb + kk;
+      if (ROW) {
+        if (ty == owner) {
+#pragma unroll
+          for (int j = 0; j < RJ; ++j) hist[k * b + tx * RJ + j] = v[kk][j];
+        }
+      } else {
+        if (tx == owner) {
+#pragma unroll
+          for (int i = 0; i < RI; ++i) hist[k * b + ty * RI + i] = v[i][kk];
+        }
+      }
+      T fxn[NF];
+      if (k + 1 < b) load_fixed(fixedg, k + 1, fx0, fxn);  // next round's fixed operand, in flight
+      __syncthreads();
+      T own[NO];
+#pragma unroll
+      for (int j = 0; j < NO; ++j) own[j] = hist[k * b + ox0 + j];
+#pragma unroll
+      for (int i = 0; i < RI; ++i)
+#pragma unroll
+        for (int j = 0; j < RJ; ++j) {
+          if (ROW) relax<T, MODE>(v[i][j], fx[i], own[j], f.int_mode, f.limit, sat);
+          else relax<T, MODE>(v[i][j], own[i], fx[j], f.int_mode, f.limit, sat);
+        }
+      if (k + 1 < b) {
+#pragma unroll
+        for (int i = 0; i < NF; ++i) fx[i] = fxn[i];
+      }
+    }
   }
 }
 
 template <class T, int MODE>
-__global__ void __launch_bounds__(kFwThreads, MODE == kChecked ? 1 : 2) fw_phase2_kernel(T* __restrict__ D, const T* __restrict__ rowsnapP,
-                                                                  const T* __restrict__ colsnapT,
-                                                                  T* __restrict__ Scol, T* __restrict__ Srow,
-                                                                  uint32_t* __restrict__ Scol16,
-                                                                  uint32_t* __restrict__ Srow16, FwArgs f) {
-  constexpr int b = FwB<T>::b, R = FwB<T>::R;
+__global__ void __launch_bounds__(kFw2Threads, MODE == kChecked ? 1 : 2)
+    fw_phase2_kernel(T* __restrict__ D, const T* __restrict__ rowsnapP, const T* __restrict__ colsnapT,
+                     T* __restrict__ Scol, T* __restrict__ Srow, uint32_t* __restrict__ Scol16,
+                     uint32_t* __restrict__ Srow16, FwArgs f) {
+  constexpr int b = FwB<T>::b, RI = Fw2<T>::RI, RJ = Fw2<T>::RJ;
   const bool row_panel = f.panel_mode == 0 ? blockIdx.y == 0 : f.panel_mode == 1;
   const int blk = row_panel ? (int)blockIdx.x : f.col_blk0 + (int)blockIdx.x;
   if (blk == (int)(f.k0 / b)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* hist = reinterpret_cast<T*>(smem_raw);  // row panel: rs[k][c]; col panel: cT[k][a]
-  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+  const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
   const int64_t r0 = row_panel ? f.k0 : (int64_t)blk * b;
   const int64_t c0 = row_panel ? (int64_t)blk * b : f.k0;
-  // row panel: fixed = colsnapT[k][a] (this thread's rows a = ty*R..);
-  // col panel: fixed = rowsnapP[k][c] (this thread's cols c = tx*R..)
-  const T* fixedg = row_panel ? colsnapT : rowsnapP;
-  const int fx0 = row_panel ? ty * R : tx * R;
-  T v[R][R];
+  T v[RI][RJ];
   load_block(D, f, r0, c0, ty, tx, v);
-  T fx[R];
-  load_fixed(fixedg, 0, fx0, fx);
   bool sat = false;
-  for (int kb = 0; kb < b; kb += R) {
-    const int owner = kb / R;
-#pragma unroll
-    for (int kk = 0; kk < R; ++kk) {
-      const int k = kb + kk;
-      if (row_panel) {
-        if (ty == owner) {
-#pragma unroll
-          for (int j = 0; j < R; ++j) hist[k * b + tx * R + j] = v[kk][j];
-        }
-      } else {
-        if (tx == owner) {
-#pragma unroll
-          for (int i = 0; i < R; ++i) hist[k * b + ty * R + i] = v[i][kk];
-        }
-      }
-      T fxn[R];
-      if (k + 1 < b) load_fixed(fixedg, k + 1, fx0, fxn);  // next round's fixed operand, in flight
-      __syncthreads();
-      T own[R];
-      const int ox = row_panel ? tx * R : ty * R;
-#pragma unroll
-      for (int j = 0; j < R; ++j) own[j] = hist[k * b + ox + j];
-      if (row_panel) {
-#pragma unroll
-        for (int i = 0; i < R; ++i)
-#pragma unroll
-          for (int j = 0; j < R; ++j) relax<T, MODE>(v[i][j], fx[i], own[j], f.int_mode, f.limit, sat);
-      } else {
-#pragma unroll
-        for (int i = 0; i < R; ++i)
-#pragma unroll
-          for (int j = 0; j < R; ++j) relax<T, MODE>(v[i][j], own[i], fx[j], f.int_mode, f.limit, sat);
-      }
-      if (k + 1 < b) {
-#pragma unroll
-        for (int i = 0; i < R; ++i) fx[i] = fxn[i];
-      }
-    }
-  }
+  if (row_panel) phase2_rounds<T, MODE, true>(v, hist, colsnapT, ty, tx, f, sat);
+  else phase2_rounds<T, MODE, false>(v, hist, rowsnapP, ty, tx, f, sat);
   store_block(D, f, r0, c0, ty, tx, v);
   __syncthreads();
   const bool out16 = row_panel ? emit_history(hist, c0, f.BNb, f, Srow, Srow16)
@@ -524,7 +538,7 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
     f.group_start = slot == 0;
     fw_phase1_kernel<T, MODE><<<1, kFw1Threads, smem1, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
     if (nblk > 1)
-      fw_phase2_kernel<T, MODE><<<dim3(nblk, 2), kFwThreads, smem2, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
+      fw_phase2_kernel<T, MODE><<<dim3(nblk, 2), kFw2Threads, smem2, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
     BTAS_CUDA_CHECK_LAUNCH();
     return BTAS_OK;
   };
@@ -685,7 +699,7 @@ int fw_dist_stage_typed(int integer_mode, int stage, T* D, int64_t ld, int64_t n
       fw_phase1_kernel<T, MODE><<<1, kFw1Threads, smem, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
       if (nblk > 1) {
         f.panel_mode = 1;
-        fw_phase2_kernel<T, MODE><<<dim3(nblk, 1), kFwThreads, smem2, st>>>(D, rsp, csp, scol, srow, scol16, srow16,
+        fw_phase2_kernel<T, MODE><<<dim3(nblk, 1), kFw2Threads, smem2, st>>>(D, rsp, csp, scol, srow, scol16, srow16,
                                                                             f);
       }
       break;
@@ -695,7 +709,7 @@ int fw_dist_stage_typed(int integer_mode, int stage, T* D, int64_t ld, int64_t n
       f.panel_mode = 2;
       f.col_blk0 = (int)(slab_r0 / b);
       const int nsb = (int)ceil_div(slab_rows, b);
-      fw_phase2_kernel<T, MODE><<<dim3(nsb, 1), kFwThreads, smem2, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
+      fw_phase2_kernel<T, MODE><<<dim3(nsb, 1), kFw2Threads, smem2, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
       break;
     }
     case BTAS_FW_STAGE_UPDATE: {
