@@ -129,28 +129,39 @@ def _peer_buffers(shape, dtype, dev, group, world):
             bufs.append(t)
             ptrs.append([a for q, a in enumerate(addrs) if q != me])
         return bufs, ptrs
-    except Exception:  # no NVLink P2P / no symmetric-memory backend
+    except Exception as exc:  # no NVLink P2P / no symmetric-memory backend
+        import os
+        import sys
+
+        if os.environ.get("BTAS_DEBUG"):
+            print(f"[btas] symmetric memory unavailable: {type(exc).__name__}: {exc}", file=sys.stderr)
         return None
 
 
 def _want_peer_exchange(group, world: int, dev: torch.device) -> bool:
     import os
 
-    # auto: fused when there is someone to exchange with; peer: always (the
-    # one-rank test of the symmetric-memory plumbing); nccl: never
+    # auto: fused when there is someone to exchange with (NCCL groups);
+    # peer: always, on any backend (the one-rank and same-GPU multi-process
+    # tests of the symmetric-memory plumbing); nccl: never
     mode = os.environ.get("BTAS_EXCHANGE", "auto")
     if mode == "nccl" or world - 1 > 7 or dev.type != "cuda" or (world < 2 and mode != "peer"):
         return False
-    return dist.get_backend(group) == "nccl"
+    return mode == "peer" or dist.get_backend(group) == "nccl"
 
 
 def apsp_by_squaring_sharded(base: torch.Tensor, group=None, gemm_rows: "Callable | None" = None,
-                             integer: bool = True, align: int = 128) -> ShardedResult:
+                             integer: bool = True, align: int = 128,
+                             peer_buffers: "Callable | None" = None) -> ShardedResult:
     """Closure of the closure base ``base`` (n x n oriented min-plus storage,
     identical on every rank) by repeated squaring, row-sharded over the
     group.  Mirrors apsp.py:136-178 step for step (fixpoint exit, counted
     detecting square, uncounted probe).  With the default CUDA ``gemm_rows``
-    on NCCL the exchange is fused into the GEMM epilogue (see module doc)."""
+    on NCCL the exchange is fused into the GEMM epilogue (see module doc).
+    ``peer_buffers(shape, dtype, device, group, world)`` may replace the
+    symmetric-memory allocation (it returns the two local buffers and, per
+    buffer, the other ranks' base addresses): the multi-process tests map
+    buffers between processes on one GPU with CUDA IPC this way."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     n = base.shape[0]
@@ -160,7 +171,8 @@ def apsp_by_squaring_sharded(base: torch.Tensor, group=None, gemm_rows: "Callabl
     chunk, spans = partition(n, world, align)
     r0, r1 = spans[rank]
 
-    peer = _peer_buffers((world * chunk, n), base.dtype, dev, group, world) if fused_ok else None
+    alloc = peer_buffers or _peer_buffers
+    peer = alloc((world * chunk, n), base.dtype, dev, group, world) if fused_ok else None
     if fused_ok:  # every rank must take the same exchange
         ok = torch.tensor([1 if peer is not None else 0], dtype=torch.int32, device=dev)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)

@@ -123,3 +123,18 @@ def test_fused_squaring_negative_cycles(cuda, golden):
         adj = bt.TropicalMatrix(MIN, sym, dtype=torch.int32)
         rep, _ = apsp_by_squaring_emulated(adj, 3)
         assert rep.negative_cycle == bool(g["meta"][case][1])
+
+
+def test_fused_exchange_across_processes(cuda):
+    """The fused exchange across real process boundaries: 2 processes on
+    this GPU, D / D_next mapped between them with CUDA IPC, gloo for the
+    host-side flag all-reduce, each rank's GEMM storing its rows into the
+    other process's D_next (tools/symm_two_proc.py)."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    tool = Path(__file__).resolve().parent.parent / "tools" / "symm_two_proc.py"
+    res = subprocess.run([sys.executable, str(tool), "2", "1100"], capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
+    assert "2-process peer-store exchange OK" in res.stdout
