@@ -71,3 +71,17 @@ def test_nccl_single_rank(cuda):
     finally:
         if created:
             dist.destroy_process_group()
+
+
+def test_distributed_fw_across_processes(cuda):
+    """floyd_warshall_distributed with 2 real processes on this GPU (gloo
+    carries the pivot-panel broadcast and reductions): identical to the
+    single-process solve (tools/fw_multi_proc.py)."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    tool = Path(__file__).resolve().parent.parent / "tools" / "fw_multi_proc.py"
+    res = subprocess.run([sys.executable, str(tool), "2"], capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
+    assert "2-process distributed Floyd-Warshall OK" in res.stdout
