@@ -212,6 +212,19 @@ size_t btas_fw_dist_workspace_bytes(int dtype, int64_t n, int64_t slab_rows, siz
 int btas_fw_dist_stage(int dtype, int integer_mode, int stage, void* D_slab, int64_t ld, int64_t n,
                        int64_t slab_r0, int64_t slab_rows, int64_t kb, int masked, double min_finite,
                        int32_t* dev_flags, void* workspace, size_t workspace_bytes, btas_stream_t stream);
+/* btas_fw_dist_stage with the pivot-panel broadcast fused into the PIVOT
+ * stage: every store the owner's phase-1 / row-panel kernels make into its
+ * broadcast region is repeated, at the same offset, in peer_regions[0..n_peers)
+ * (n_peers <= 7): the other ranks' broadcast regions (their workspace +
+ * bcast_offset) mapped into this process (NVLink peer memory / CUDA IPC).
+ * The caller replaces the broadcast by a barrier that orders the peers'
+ * COLS stage after this PIVOT stage, and alternates two workspaces by the
+ * parity of kb so the next owner's stores never overwrite a region a peer is
+ * still reading.  Other stages ignore the peers. */
+int btas_fw_dist_stage_peers(int dtype, int integer_mode, int stage, void* D_slab, int64_t ld, int64_t n,
+                             int64_t slab_r0, int64_t slab_rows, int64_t kb, int masked, double min_finite,
+                             int32_t* dev_flags, void* workspace, size_t workspace_bytes,
+                             void* const* peer_regions, int n_peers, btas_stream_t stream);
 
 /* Diagonal test: sets BTAS_FLAG_DIAG_NEG if any d[i,i] < 0 (apsp.py:125,168). */
 int btas_diag_negative(int dtype, const void* d, int64_t ld, int64_t n, int32_t* dev_flags,

@@ -87,9 +87,7 @@ BTAS_D uint32_t s16_lane(T v) {
 template <class T>
 struct FwB {
   static constexpr int b = sizeof(T) == 8 ? 64 : 128;  // pivot block (phase-3 K)
-  static constexpr int R = b / 16;                      // per-thread sub-block edge (16 x 16 threads)
 };
-constexpr int kFwThreads = 256;
 
 struct FwArgs {
   int64_t n, ld, k0;
@@ -109,13 +107,44 @@ struct FwArgs {
   int emit_s16;      // also emit the int16x2 operands
   int32_t* flags;
   FwCtrl* ctrl;
+  // fused pivot-panel broadcast (distributed FW): every store into this
+  // rank's broadcast region [region_lo, region_hi) is repeated at the same
+  // offset in up to 7 peers' regions (the other ranks' workspaces, mapped
+  // over NVLink / CUDA IPC), so the panel reaches them as it is produced
+  unsigned char* region_lo;
+  unsigned char* region_hi;
+  unsigned char* peer_region[7];
+  int n_peers;
 };
 
-// The tile lives in registers: thread (ty, tx) of a 16 x 16 grid owns rows
-// ty*R .. +R and cols tx*R .. +R.  Round k: the owners of row k / column k
-// publish the PRE-round values into the history arrays (which double as the
-// round's operand buffers — written once, so one barrier per round), then
-// every thread relaxes its R x R block.
+// store v at p, and at the same region offset in every peer's workspace
+template <class V>
+BTAS_D void rstore(const FwArgs& f, V* p, V v) {
+  *p = v;
+  if (f.n_peers > 0) {
+    const unsigned char* a = reinterpret_cast<const unsigned char*>(p);
+    if (a >= f.region_lo && a < f.region_hi) {
+      const size_t off = (size_t)(a - f.region_lo);
+      for (int q = 0; q < f.n_peers; ++q) *reinterpret_cast<V*>(f.peer_region[q] + off) = v;
+    }
+  }
+}
+BTAS_D void rflag_or(const FwArgs& f, int32_t* p) {
+  atomicOr(p, 1);
+  if (f.n_peers > 0) {
+    const unsigned char* a = reinterpret_cast<const unsigned char*>(p);
+    if (a >= f.region_lo && a < f.region_hi) {
+      const size_t off = (size_t)(a - f.region_lo);
+      for (int q = 0; q < f.n_peers; ++q) atomicOr_system(reinterpret_cast<int32_t*>(f.peer_region[q] + off), 1);
+    }
+  }
+}
+
+// The tile lives in registers: thread (ty, tx) owns rows ty*RI .. +RI and
+// cols tx*RJ .. +RJ (phase 1: 32 x 32 threads, phase 2: 16 x 32).  Round k:
+// the owners of row k / column k publish the PRE-round values into the
+// history arrays (which double as the round's operand buffers — written
+// once, so one barrier per round), then every thread relaxes its block.
 template <class T, int RI, int RJ>
 BTAS_D void load_block(const T* __restrict__ D, const FwArgs& f, int64_t r0, int64_t c0, int ty, int tx,
                        T (&v)[RI][RJ]) {
@@ -156,8 +185,8 @@ BTAS_D bool emit_history(const T* __restrict__ h, int64_t rc0, int BLK, const Fw
     const int kp = e / b, x = e - kp * b;
     const T v0 = h[(2 * kp) * b + x], v1 = h[(2 * kp + 1) * b + x];
     const int64_t idx = packed_index(rc0 + x, f.koff + 2 * kp, f.Kp2, BLK);
-    P[idx] = v0;
-    P[idx + 1] = v1;
+    rstore(f, P + idx, v0);
+    rstore(f, P + idx + 1, v1);
     out16 |= !s16_ok(v0) || !s16_ok(v1);
   }
   if (f.emit_s16) {
@@ -167,8 +196,8 @@ BTAS_D bool emit_history(const T* __restrict__ h, int64_t rc0, int BLK, const Fw
       const uint32_t w0 = s16_lane(h[k * b + x]) | (s16_lane(h[(k + 1) * b + x]) << 16);
       const uint32_t w1 = s16_lane(h[(k + 2) * b + x]) | (s16_lane(h[(k + 3) * b + x]) << 16);
       const int64_t idx = packed_index(rc0 + x, f.koff / 2 + 2 * wp, f.Kp2w, 128);
-      P16[idx] = w0;
-      P16[idx + 1] = w1;
+      rstore(f, P16 + idx, w0);
+      rstore(f, P16 + idx + 1, w1);
     }
   }
   return out16;
@@ -191,7 +220,7 @@ __global__ void __launch_bounds__(kFw1Threads) fw_phase1_kernel(T* __restrict__ 
   T* cT = rs + b * b;
   const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    if (f.group_start) f.ctrl->s16_overflow[0] = 0;
+    if (f.group_start) rstore(f, &f.ctrl->s16_overflow[0], 0);
   }
   T v[R][R];
   load_block(D, f, f.k0, f.k0, ty, tx, v);
@@ -224,14 +253,14 @@ __global__ void __launch_bounds__(kFw1Threads) fw_phase1_kernel(T* __restrict__ 
   store_block(D, f, f.k0, f.k0, ty, tx, v);
   __syncthreads();
   for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
-    rowsnapP[e] = rs[e];
-    colsnapT[e] = cT[e];
+    rstore(f, rowsnapP + e, rs[e]);
+    rstore(f, colsnapT + e, cT[e]);
   }
   // pivot rows of Scol (A operand) and pivot columns of Srow (B operand)
   bool out16 = emit_history(cT, f.k0 - f.slab_r0, f.BMa, f, Scol, Scol16);  // Scol rows are slab-local
   out16 |= emit_history(rs, f.k0, f.BNb, f, Srow, Srow16);
   if (__syncthreads_or(out16) && threadIdx.x == 0) {
-    atomicOr(&f.ctrl->s16_overflow[0], 1);
+    rflag_or(f, &f.ctrl->s16_overflow[0]);
   }
   if (MODE == kChecked && __any_sync(0xffffffffu, sat) && (threadIdx.x & 31) == 0)
     atomicOr(&f.flags[BTAS_FLAG_SATURATED], 1);
@@ -346,7 +375,7 @@ __global__ void __launch_bounds__(kFw2Threads, MODE == kChecked ? 1 : 2)
   const bool out16 = row_panel ? emit_history(hist, c0, f.BNb, f, Srow, Srow16)
                                : emit_history(hist, r0 - f.slab_r0, f.BMa, f, Scol, Scol16);
   if (__syncthreads_or(out16) && threadIdx.x == 0) {
-    atomicOr(&f.ctrl->s16_overflow[0], 1);
+    rflag_or(f, &f.ctrl->s16_overflow[0]);
   }
   if (MODE == kChecked && __any_sync(0xffffffffu, sat) && (threadIdx.x & 31) == 0)
     atomicOr(&f.flags[BTAS_FLAG_SATURATED], 1);
@@ -635,7 +664,8 @@ FwDistWs fw_dist_ws(int64_t n, int64_t slab_rows) {
 
 template <class T, int MODE>
 int fw_dist_stage_typed(int integer_mode, int stage, T* D, int64_t ld, int64_t n, int64_t slab_r0, int64_t slab_rows,
-                        int64_t kb, int32_t* flags, unsigned char* ws, cudaStream_t st) {
+                        int64_t kb, int32_t* flags, unsigned char* ws, void* const* peers, int n_peers,
+                        cudaStream_t st) {
   using G = FwGeom<T>;
   constexpr int b = G::b;
   constexpr bool CHECKED = MODE == kChecked;
@@ -671,6 +701,10 @@ int fw_dist_stage_typed(int integer_mode, int stage, T* D, int64_t ld, int64_t n
   f.emit_s16 = emit_s16 ? 1 : 0;
   f.flags = flags;
   f.ctrl = ctrl;
+  f.region_lo = ws + W.ctrl;
+  f.region_hi = ws + W.bcast_end;
+  f.n_peers = n_peers;
+  for (int q = 0; q < n_peers; ++q) f.peer_region[q] = static_cast<unsigned char*>(peers[q]);
   const size_t smem = 2 * (size_t)b * b * sizeof(T);
   const size_t smem2 = (size_t)b * b * sizeof(T);
   static bool configured = false;
@@ -846,11 +880,15 @@ extern "C" size_t btas_fw_dist_workspace_bytes(int dtype, int64_t n, int64_t sla
   return total;
 }
 
-extern "C" int btas_fw_dist_stage(int dtype, int integer_mode, int stage, void* D_slab, int64_t ld, int64_t n,
-                                  int64_t slab_r0, int64_t slab_rows, int64_t kb, int masked, double min_finite,
-                                  int32_t* dev_flags, void* workspace, size_t workspace_bytes, btas_stream_t stream) {
+static int fw_dist_stage_entry(int dtype, int integer_mode, int stage, void* D_slab, int64_t ld, int64_t n,
+                               int64_t slab_r0, int64_t slab_rows, int64_t kb, int masked, double min_finite,
+                               int32_t* dev_flags, void* workspace, size_t workspace_bytes, void* const* peers,
+                               int n_peers, btas_stream_t stream) {
   if (!dev_flags || !workspace || n < 1 || ld < n || slab_r0 < 0 || slab_rows < 0 || slab_r0 + slab_rows > n)
     return BTAS_ERR_INVALID;
+  if (n_peers < 0 || n_peers > 7 || (n_peers > 0 && !peers)) return BTAS_ERR_INVALID;
+  for (int q = 0; q < n_peers; ++q)
+    if (!peers[q]) return BTAS_ERR_INVALID;
   if (slab_rows > 0 && !D_slab) return BTAS_ERR_INVALID;
   const int64_t b = dtype == BTAS_F64 ? 64 : 128;
   if ((slab_rows > 0 && slab_r0 % 128 != 0) || kb < 0 || kb * b >= n) return BTAS_ERR_INVALID;
@@ -859,12 +897,12 @@ extern "C" int btas_fw_dist_stage(int dtype, int integer_mode, int stage, void* 
   unsigned char* ws = static_cast<unsigned char*>(workspace);
 #define BTAS_FWD_CALL(T)                                                                                          \
   (masked ? fw_dist_stage_typed<T, kChecked>(integer_mode, stage, (T*)D_slab, ld, n, slab_r0, slab_rows, kb,      \
-                                             dev_flags, ws, st)                                                   \
+                                             dev_flags, ws, peers, n_peers, st)                                   \
    : (dtype == BTAS_I32 && min_finite < 0.0)                                                                      \
        ? fw_dist_stage_typed<T, kClamp>(integer_mode, stage, (T*)D_slab, ld, n, slab_r0, slab_rows, kb, dev_flags, \
-                                        ws, st)                                                                   \
+                                        ws, peers, n_peers, st)                                                   \
        : fw_dist_stage_typed<T, kFast>(integer_mode, stage, (T*)D_slab, ld, n, slab_r0, slab_rows, kb, dev_flags,  \
-                                       ws, st))
+                                       ws, peers, n_peers, st))
   switch (dtype) {
     case BTAS_F32:
       return BTAS_FWD_CALL(float);
@@ -876,4 +914,20 @@ extern "C" int btas_fw_dist_stage(int dtype, int integer_mode, int stage, void* 
       return BTAS_ERR_INVALID;
   }
 #undef BTAS_FWD_CALL
+}
+
+extern "C" int btas_fw_dist_stage(int dtype, int integer_mode, int stage, void* D_slab, int64_t ld, int64_t n,
+                                  int64_t slab_r0, int64_t slab_rows, int64_t kb, int masked, double min_finite,
+                                  int32_t* dev_flags, void* workspace, size_t workspace_bytes, btas_stream_t stream) {
+  return fw_dist_stage_entry(dtype, integer_mode, stage, D_slab, ld, n, slab_r0, slab_rows, kb, masked, min_finite,
+                             dev_flags, workspace, workspace_bytes, nullptr, 0, stream);
+}
+
+extern "C" int btas_fw_dist_stage_peers(int dtype, int integer_mode, int stage, void* D_slab, int64_t ld, int64_t n,
+                                        int64_t slab_r0, int64_t slab_rows, int64_t kb, int masked,
+                                        double min_finite, int32_t* dev_flags, void* workspace,
+                                        size_t workspace_bytes, void* const* peer_regions, int n_peers,
+                                        btas_stream_t stream) {
+  return fw_dist_stage_entry(dtype, integer_mode, stage, D_slab, ld, n, slab_r0, slab_rows, kb, masked, min_finite,
+                             dev_flags, workspace, workspace_bytes, peer_regions, n_peers, stream);
 }

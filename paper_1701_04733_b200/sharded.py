@@ -308,39 +308,66 @@ FW_STAGE_INIT, FW_STAGE_PIVOT, FW_STAGE_COLS, FW_STAGE_UPDATE, FW_STAGE_DIAG = 0
 
 
 class _FwRank:
-    """One rank's slab, workspace and flag words for btas_fw_dist_stage."""
+    """One rank's slab, workspace(s) and flag words for btas_fw_dist_stage.
+    With the fused broadcast the rank holds two workspaces, alternated by the
+    parity of the pivot block (``alloc(nbytes)`` may place them in memory the
+    peers can map)."""
 
-    def __init__(self, rank, r0, rows, slab, code, n, dev):
+    def __init__(self, rank, r0, rows, slab, code, n, dev, nbuf=1, alloc=None):
         import ctypes
 
         self.rank, self.r0, self.rows, self.slab = rank, r0, rows, slab
         off, nb = ctypes.c_size_t(), ctypes.c_size_t()
         total = _lib.load().btas_fw_dist_workspace_bytes(code, n, rows, ctypes.byref(off), ctypes.byref(nb))
-        self.ws = torch.empty(total, dtype=torch.uint8, device=dev)
-        self.region = self.ws[off.value : off.value + nb.value]
+        self.total, self.region_off, self.region_bytes = total, off.value, nb.value
+        self.wss = [alloc(total) if alloc is not None else torch.empty(total, dtype=torch.uint8, device=dev)
+                    for _ in range(nbuf)]
         self.flags = torch.zeros(_lib.NUM_FLAGS, dtype=torch.int32, device=dev)
 
+    def ws(self, kb: int) -> torch.Tensor:
+        return self.wss[kb % len(self.wss)]
 
-def _fw_rows_run(ranks, code, integer, n, ld, masked, min_fin, b, chunk, bcast):
+    def region(self, kb: int = 0) -> torch.Tensor:
+        return self.ws(kb)[self.region_off : self.region_off + self.region_bytes]
+
+
+def _fw_rows_run(ranks, code, integer, n, ld, masked, min_fin, b, chunk, bcast, peers=None):
     """The stage sequence of btas_fw_dist_stage (include/btas_cuda.h) over
-    the given local ranks; ``bcast(owner, ranks)`` moves the owner's
-    broadcast region to every rank."""
+    the given local ranks; ``bcast(owner, ranks, kb)`` moves the owner's
+    broadcast region to every rank.  With ``peers(kb, rank) -> [addresses]``
+    the owner's PIVOT stage stores its region into the peers' regions itself
+    (btas_fw_dist_stage_peers) and ``bcast`` is only the barrier (also called
+    once with owner -1 after the INIT stages)."""
+    import ctypes
+
     from .matrix import _ptr, _stream
 
-    def stage(rk, s, kb=0):
+    def stage(rk, s, kb=0, buf=None):
+        ws = rk.ws(kb if buf is None else buf)
         ptr = _ptr(rk.slab) if rk.rows > 0 else None
-        _lib.call("btas_fw_dist_stage", code, 1 if integer else 0, s, ptr, ld, n, rk.r0, rk.rows, kb,
-                  1 if masked else 0, min_fin, _ptr(rk.flags), _ptr(rk.ws), rk.ws.numel(), _stream(rk.ws.device))
+        args = (code, 1 if integer else 0, s, ptr, ld, n, rk.r0, rk.rows, kb, 1 if masked else 0, min_fin,
+                _ptr(rk.flags), _ptr(ws), ws.numel())
+        pr = peers(kb, rk.rank) if (peers is not None and s == FW_STAGE_PIVOT) else None
+        if pr:
+            arr = (ctypes.c_void_p * len(pr))(*pr)
+            _lib.call("btas_fw_dist_stage_peers", *args, arr, len(pr), _stream(ws.device))
+        else:
+            _lib.call("btas_fw_dist_stage", *args, _stream(ws.device))
 
     for rk in ranks:
-        stage(rk, FW_STAGE_INIT)
+        for i in range(len(rk.wss)):
+            stage(rk, FW_STAGE_INIT, 0, buf=i)
+    if peers is not None:
+        # the peers' INIT (padding fill of their regions) must finish before
+        # any owner stores a panel into them
+        bcast(-1, ranks, -1)
     nblk = -(-n // b)
     for kb in range(nblk):
         owner = (kb * b) // chunk
         for rk in ranks:
             if rk.rank == owner:
                 stage(rk, FW_STAGE_PIVOT, kb)
-        bcast(owner, ranks)
+        bcast(owner, ranks, kb)
         for rk in ranks:
             stage(rk, FW_STAGE_COLS, kb)
         for rk in ranks:
@@ -386,14 +413,33 @@ def _fw_report(adj, d, negative):
                       negative_cycle=negative, multiplications_performed=0)
 
 
-def floyd_warshall_distributed(adj, group=None):
+def _fw_peer_workspaces(nbytes, dev, group, world):
+    """Two symmetric-memory workspaces and, per workspace, the other ranks'
+    base addresses (None when symmetric memory is unavailable)."""
+    got = _peer_buffers((nbytes,), torch.uint8, dev, group, world)
+    return got
+
+
+def floyd_warshall_distributed(adj, group=None, peer_workspaces=None):
     """``floyd_warshall`` (reference apsp.py:93-133) with D row-sharded over
-    the ranks of ``group`` (one process per GPU, NCCL): per pivot block the
-    owning rank computes the pivot tile and row panel, broadcasts the packed
-    row-panel snapshots (b x n) over NVLink, and every rank updates its own
-    rows.  Every rank passes the same adjacency and receives the full result;
-    distances and the negative-cycle flag are byte-identical to the
-    single-GPU ``floyd_warshall`` for any number of ranks."""
+    the ranks of ``group`` (one process per GPU): per pivot block the owning
+    rank computes the pivot tile and the row panel, every rank receives the
+    packed row-panel snapshots (b x n), and every rank updates its own rows.
+
+    On NCCL groups the panel distribution is **fused into the owner's
+    kernels**: the workspaces live in symmetric memory and the phase-1 /
+    row-panel kernels store every snapshot into the peers' broadcast regions
+    as they produce it (btas_fw_dist_stage_peers); a one-word all-reduce then
+    orders the peers' column panels after it, and two workspaces alternate by
+    pivot-block parity so the next owner never overwrites a region a peer is
+    still reading.  Otherwise (``BTAS_EXCHANGE=nccl``, no symmetric memory)
+    the owner's region goes out with one NCCL broadcast per block.
+    ``peer_workspaces(nbytes, device, group, world)`` may replace the
+    symmetric-memory allocation (multi-process tests on one GPU map the
+    workspaces with CUDA IPC).  Every rank passes the same adjacency and
+    receives the full result; distances and the negative-cycle flag are
+    byte-identical to the single-GPU ``floyd_warshall`` for any number of
+    ranks."""
     from .semiring import _note_saturation
 
     n, base, code, b, limit = _fw_setup(adj)
@@ -402,6 +448,7 @@ def floyd_warshall_distributed(adj, group=None):
     chunk, spans = partition(n, world)
     r0, r1 = spans[rank]
     d = base.data
+    dev = d.device
     ld = d.stride(0)
     st = _slab_stats(d[r0:r1], code)
     mx = st[:1].clone()
@@ -410,17 +457,42 @@ def floyd_warshall_distributed(adj, group=None):
     dist.all_reduce(mn, op=dist.ReduceOp.MIN, group=group)
     max_abs, min_fin = float(mx.item()), float(mn.item())
     masked = not (2.0 * (n + 1) * max_abs < limit)
-    rk = _FwRank(rank, r0, r1 - r0, d[r0:r1], code, n, d.device)
 
-    def bcast(owner, ranks):
-        dist.broadcast(ranks[0].region, src=dist.get_global_rank(group, owner) if group is not None else owner,
-                       group=group)
+    fused = peer_workspaces is not None or _want_peer_exchange(group, world, dev)
+    rk, peer_ptrs = None, None
+    if fused:
+        probe = _FwRank(rank, r0, r1 - r0, d[r0:r1], code, n, dev, nbuf=0)
+        got = (peer_workspaces or _fw_peer_workspaces)(probe.total, dev, group, world)
+        ok = torch.tensor([1 if got is not None else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)  # every rank takes the same route
+        if int(_host_read(ok)[0]) and got is not None:
+            bufs, bases = got
+            it = iter(bufs)
+            rk = _FwRank(rank, r0, r1 - r0, d[r0:r1], code, n, dev, nbuf=2, alloc=lambda nbytes: next(it))
+            peer_ptrs = [[a + rk.region_off for a in per_buf] for per_buf in bases]
+    if rk is None:
+        rk = _FwRank(rank, r0, r1 - r0, d[r0:r1], code, n, dev)
 
-    _fw_rows_run([rk], code, base.integer, n, ld, masked, min_fin, b, chunk, bcast)
+    if peer_ptrs is not None:
+        token = torch.zeros(1, dtype=torch.int32, device=dev)
+
+        def bcast(owner, ranks, kb):  # the owner's kernels already stored the panel into the peers
+            dist.all_reduce(token, op=dist.ReduceOp.MAX, group=group)
+
+        def peers(kb, r):
+            return peer_ptrs[kb % 2]
+    else:
+        def bcast(owner, ranks, kb):
+            dist.broadcast(ranks[0].region(kb), src=dist.get_global_rank(group, owner) if group is not None else owner,
+                           group=group)
+
+        peers = None
+
+    _fw_rows_run([rk], code, base.integer, n, ld, masked, min_fin, b, chunk, bcast, peers)
     flags = rk.flags.clone()
     dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=group)
     # gather the row slabs into the full distance matrix on every rank
-    full = torch.empty((world * chunk, n), dtype=d.dtype, device=d.device)
+    full = torch.empty((world * chunk, n), dtype=d.dtype, device=dev)
     mine = full[rank * chunk : (rank + 1) * chunk]
     if r1 > r0:
         mine[: r1 - r0].copy_(d[r0:r1])
@@ -431,12 +503,13 @@ def floyd_warshall_distributed(adj, group=None):
     return _fw_report(adj, full[:n].contiguous() if world * chunk != n else full, bool(f[_lib.FLAG_DIAG_NEG]))
 
 
-def floyd_warshall_emulated(adj, world: int):
+def floyd_warshall_emulated(adj, world: int, fused: bool = False):
     """The row-sharded program of ``floyd_warshall_distributed`` with
     ``world`` virtual ranks executed in sequence on ONE GPU (slabs are row
-    ranges of one matrix, the broadcast is a device copy).  Exercises the
-    exact per-rank stage sequence and slab indexing of P > 1 where only one
-    GPU is available; the result must equal the single-GPU solve."""
+    ranges of one matrix).  ``fused=False``: the broadcast is a device copy;
+    ``fused=True``: the owner's PIVOT kernels store the panel into the other
+    virtual ranks' (double-buffered) workspaces at exactly the addresses the
+    multi-GPU path uses.  The result must equal the single-GPU solve."""
     from .semiring import _note_saturation
 
     n, base, code, b, limit = _fw_setup(adj)
@@ -447,15 +520,25 @@ def floyd_warshall_emulated(adj, world: int):
     max_abs = max(float(s[0]) for s in st)
     min_fin = min(float(s[1]) for s in st)
     masked = not (2.0 * (n + 1) * max_abs < limit)
-    ranks = [_FwRank(r, r0, r1 - r0, d[r0:r1], code, n, d.device) for r, (r0, r1) in enumerate(spans)]
+    nbuf = 2 if fused else 1
+    ranks = [_FwRank(r, r0, r1 - r0, d[r0:r1], code, n, d.device, nbuf=nbuf) for r, (r0, r1) in enumerate(spans)]
 
-    def bcast(owner, rks):
-        src = rks[owner].region
-        for rk in rks:
-            if rk.rank != owner:
-                rk.region.copy_(src)
+    if fused:
+        def bcast(owner, rks, kb):
+            pass
 
-    _fw_rows_run(ranks, code, base.integer, n, ld, masked, min_fin, b, chunk, bcast)
+        def peers(kb, r):
+            return [rk.region(kb).data_ptr() for rk in ranks if rk.rank != r]
+    else:
+        def bcast(owner, rks, kb):
+            src = rks[owner].region(kb)
+            for rk in rks:
+                if rk.rank != owner:
+                    rk.region(kb).copy_(src)
+
+        peers = None
+
+    _fw_rows_run(ranks, code, base.integer, n, ld, masked, min_fin, b, chunk, bcast, peers)
     f = torch.stack([rk.flags for rk in ranks]).amax(dim=0).cpu().tolist()
     if f[_lib.FLAG_SATURATED]:
         _note_saturation()

@@ -24,11 +24,14 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("dtype", DTYPES)
 @pytest.mark.parametrize("world", [1, 2, 3, 5])
-def test_emulated_ranks_match_single_gpu(cuda, dtype, world):
+@pytest.mark.parametrize("fused", [False, True])
+def test_emulated_ranks_match_single_gpu(cuda, dtype, world, fused):
+    """fused=True: the owner's PIVOT kernels store the panel straight into the
+    other virtual ranks' double-buffered workspaces (btas_fw_dist_stage_peers)."""
     for n, p, wr, seed in ((700, 0.5, (1, 100), 1), (333, 0.05, (0, 60), 2), (130, 0.4, (-1, 40), 3), (1, 0.5, (1, 2), 4)):
         adj = random_graph_matrix(n, p, wr, seed, dtype=dtype)
         want = bt.floyd_warshall(adj)
-        got = floyd_warshall_emulated(adj, world)
+        got = floyd_warshall_emulated(adj, world, fused=fused)
         assert got.negative_cycle == want.negative_cycle
         if not want.negative_cycle:
             assert got.distances.dist == want.distances.dist, (n, world)
@@ -41,6 +44,7 @@ def test_emulated_negative_cycles_and_masked(cuda, golden):
         sym[np.isinf(sym)] = math.inf
         adj = bt.TropicalMatrix(MIN, sym, dtype=torch.int32)
         assert floyd_warshall_emulated(adj, 2).negative_cycle == bool(g["meta"][case][1])
+        assert floyd_warshall_emulated(adj, 3, fused=True).negative_cycle == bool(g["meta"][case][1])
     rng = np.random.default_rng(8)
     n = 300
     sym = rng.integers(1, 10**7, (n, n)).astype(float)
