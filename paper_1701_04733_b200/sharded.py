@@ -437,9 +437,9 @@ def floyd_warshall_distributed(adj, group=None, peer_workspaces=None):
     ``peer_workspaces(nbytes, device, group, world)`` may replace the
     symmetric-memory allocation (multi-process tests on one GPU map the
     workspaces with CUDA IPC).  Every rank passes the same adjacency and
-    receives the full result; distances and the negative-cycle flag are
-    byte-identical to the single-GPU ``floyd_warshall`` for any number of
-    ranks."""
+    receives the full result; the negative-cycle flag, and the distances of
+    every graph without a negative cycle, are byte-identical to the
+    single-GPU ``floyd_warshall`` for any number of ranks."""
     from .semiring import _note_saturation
 
     n, base, code, b, limit = _fw_setup(adj)
