@@ -554,7 +554,7 @@ def apsp_arm(args, rank, world, dev):
         # GEMM epilogue (peer stores into symmetric memory), NCCL fallback
         from paper_1701_04733_b200.sharded import apsp_by_squaring_distributed as solver  # noqa: F811
     elif args.workload == "fw" and world > 1:
-        # row-sharded blocked FW, NCCL broadcast of the pivot row panel per block
+        # row-sharded blocked FW; the pivot panel is stored into the peers by the owner's kernels
         from paper_1701_04733_b200.sharded import floyd_warshall_distributed as solver  # noqa: F811
     for _ in range(max(1, min(args.warmup, 3))):
         rep = solver(adj)
@@ -585,9 +585,57 @@ def apsp_arm(args, rank, world, dev):
                       "gpairs_per_s": round(pairs / (ms * 1e-3) / 1e9, 1)}}
     if args.workload == "apsp" and world > 1:
         res["config"]["exchange"] = os.environ.get("BTAS_EXCHANGE", "auto")
+    # roofline: the add-min pairs of the whole solve against the live
+    # ceiling of the s16x2 mix the integer-valued instances run on
+    from paper_1701_04733_b200 import _lib
+
+    probe = _lib.probe_ceiling(2)
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak = probe["pairs_per_clk_sm"] * nsm * probe["sm_mhz"] * 1e6 / 1e12 * world
+    ach = pairs / (ms * 1e-3) / 1e12
+    res["roofline"] = {"bound": "alu", "achieved": round(ach, 3), "peak": round(peak, 3), "unit": "Tpair/s",
+                       "frac": round(ach / peak, 4), "traffic": None,
+                       "peak_source": "btas_probe_ceiling(s16x2) x SMs x probe clock x GPUs",
+                       "work": "n^3 pairs (FW) / multiplications x n^3 (squaring), whole solve"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        res["cpu_baseline"] = apsp_cpu_baseline(args.workload, n)
     if rank == 0:
         print(json.dumps(res), flush=True)
     return 0
+
+
+def apsp_cpu_baseline(workload, n):
+    """The reference's CPU algorithm on the host (oracle restatement, NumPy):
+    C1 squaring in full; FW as a few k-rounds of the n' <= 4096 leading
+    sub-instance (the reference round: d = min(d, d[:, k] (+) d[k, :])),
+    extrapolated as n'^2 per round x n rounds x (n / n')^2."""
+    import numpy as np
+
+    from oracle import tropical as ot
+    from paper_1701_04733_b200.graphs import dense_rows, instance_seed
+
+    cores = len(os.sched_getaffinity(0))
+    if workload == "apsp" and n <= 2048:
+        sym = np.concatenate([blk for _, blk in dense_rows(n, 0.5, (1, 100), instance_seed(1, n))])
+        ot.apsp_by_squaring(sym[:64, :64], "f32", True)  # warm-up
+        t = time.perf_counter()
+        ot.apsp_by_squaring(sym, "f32", True)
+        secs = time.perf_counter() - t
+        return {"value": round(secs, 4), "unit": "s", "cores": cores, "kind": "port",
+                "sample": f"the full n={n} instance, NumPy restatement of apsp_by_squaring (threaded products)"}
+    sub = min(n, 4096)
+    rows = [blk for r0, blk in dense_rows(n, 0.5, (1, 100), instance_seed(1, n), chunk_rows=1024) if r0 < sub]
+    d = np.ascontiguousarray(np.concatenate(rows)[:sub, :sub])
+    np.fill_diagonal(d, np.minimum(np.diagonal(d), 0.0))
+    rounds = 4
+    t = time.perf_counter()
+    for k in range(rounds):
+        np.minimum(d, np.add.outer(d[:, k], d[k, :]), out=d)
+    per_round = (time.perf_counter() - t) / rounds
+    secs = per_round * (n / sub) ** 2 * n
+    return {"value": round(secs, 1), "unit": "s", "cores": 1, "kind": "port",
+            "sample": f"{rounds} reference FW rounds on the leading {sub}x{sub} block ({per_round:.3f} s/round), "
+                      f"extrapolated x (n/{sub})^2 per round x n rounds"}
 
 
 def hbm_arm(args, rank, world, dev):
