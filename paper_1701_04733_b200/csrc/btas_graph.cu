@@ -22,6 +22,7 @@
 //             0, absent +inf) through the same float64 -> storage conversion
 //             and statistics as btas_ingest
 #include <algorithm>
+#include <cmath>
 #include <type_traits>
 
 #include "btas_common.cuh"
@@ -264,7 +265,17 @@ __global__ void __launch_bounds__(kGenThreads) draw_kernel(const __grid_constant
 }
 
 // ------------------------------------------------------------------ fill
+// integer weights whose every value is representable exactly (int32:
+// |w| < 2^28; float storage: |w| < 2^53): the stored value is a plain
+// conversion and every statistic btas_ingest would report is zero, so the
+// fast variant skips the per-element validation entirely
 template <class D>
+BTAS_D D store_int_weight(int64_t w) {
+  if constexpr (Traits<D>::dtype == BTAS_I32) return (D)w;
+  else return (D)(double)w;  // numpy astype(float64), then the storage rounding
+}
+
+template <class D, bool FAST>
 __global__ void __launch_bounds__(kGenThreads) fill_kernel(int64_t n, int wmode, bool wide, int64_t low,
                                                            const void* __restrict__ draws, D* __restrict__ out,
                                                            int64_t ld, const uint32_t* __restrict__ bits,
@@ -276,7 +287,10 @@ __global__ void __launch_bounds__(kGenThreads) fill_kernel(int64_t n, int wmode,
   const D inf = Traits<D>::eps(true);
   const int lane = threadIdx.x & 31;
   const int64_t gtid = (int64_t)blockIdx.x * kGenThreads + threadIdx.x;
-  if (gtid < n) out[gtid * ld + gtid] = ingest_one<double, D, A>(0.0, inf, st);  // graph_to_matrix diagonal
+  if (gtid < n) {  // graph_to_matrix diagonal
+    if constexpr (FAST) out[gtid * ld + gtid] = (D)0;
+    else out[gtid * ld + gtid] = ingest_one<double, D, A>(0.0, inf, st);
+  }
   const uint64_t pairs = (uint64_t)n * (uint64_t)(n - 1);
   const uint64_t w0 = (uint64_t)blockIdx.x * kCtaUnits + (uint64_t)(threadIdx.x >> 5) * kWarpUnits;
   if (blockIdx.x < ctas && w0 < pairs) {
@@ -293,20 +307,35 @@ __global__ void __launch_bounds__(kGenThreads) fill_kernel(int64_t n, int wmode,
       const uint64_t q = q0 + 32ull * it;
       if (q < pairs) {
         const bool present = (b >> lane) & 1u;
-        double w = INFINITY;
-        if (present) {
-          const int64_t m = rank + warp_excl(b);
-          if (wmode == BTAS_WEIGHTS_CONST) {
-            w = (double)low;
-          } else if (wmode == BTAS_WEIGHTS_UNIFORM) {
-            w = static_cast<const double*>(draws)[m];
-          } else {
-            const uint64_t v = wide ? static_cast<const uint64_t*>(draws)[m]
-                                    : (uint64_t) static_cast<const uint32_t*>(draws)[m];
-            w = (double)(int64_t)((uint64_t)low + v);  // numpy: off + draw, then astype(float64)
+        D val;
+        if constexpr (FAST) {
+          val = inf;
+          if (present) {
+            int64_t w = low;
+            if (wmode == BTAS_WEIGHTS_BOUNDED) {
+              const int64_t m = rank + warp_excl(b);
+              w = (int64_t)((uint64_t)low + (wide ? static_cast<const uint64_t*>(draws)[m]
+                                                  : (uint64_t) static_cast<const uint32_t*>(draws)[m]));
+            }
+            val = store_int_weight<D>(w);
           }
+        } else {
+          double w = INFINITY;
+          if (present) {
+            const int64_t m = rank + warp_excl(b);
+            if (wmode == BTAS_WEIGHTS_CONST) {
+              w = (double)low;
+            } else if (wmode == BTAS_WEIGHTS_UNIFORM) {
+              w = static_cast<const double*>(draws)[m];
+            } else {
+              const uint64_t v = wide ? static_cast<const uint64_t*>(draws)[m]
+                                      : (uint64_t) static_cast<const uint32_t*>(draws)[m];
+              w = (double)(int64_t)((uint64_t)low + v);  // numpy: off + draw, then astype(float64)
+            }
+          }
+          val = ingest_one<double, D, A>(w, inf, st);
         }
-        out[row * ld + j + (j >= row ? 1 : 0)] = ingest_one<double, D, A>(w, inf, st);
+        out[row * ld + j + (j >= row ? 1 : 0)] = val;
       }
       rank += __popc(b);
       j += 32;
@@ -316,7 +345,7 @@ __global__ void __launch_bounds__(kGenThreads) fill_kernel(int64_t n, int wmode,
       }
     }
   }
-  commit(st, stats);
+  if constexpr (!FAST) commit(st, stats);
 }
 
 // ------------------------------------------------------------------ edge lists
@@ -557,25 +586,38 @@ extern "C" int btas_graph_fill(int dtype, const btas_pcg64* rng, int64_t n, uint
   const bool wide = weights_mode == BTAS_WEIGHTS_BOUNDED && range > 0xFFFFFFFFull;
   const int64_t grid = std::max<int64_t>(w.p_ctas, ceil_div(n, kGenThreads));
   if (grid > 0x7FFFFFFF) return BTAS_ERR_UNSUPPORTED;
+  // the fast fill needs integer weights that every storage holds exactly
+  const int64_t hi = weights_mode == BTAS_WEIGHTS_BOUNDED ? (int64_t)((uint64_t)low + range) : low;
+  const double mag = std::max(std::fabs((double)low), std::fabs((double)hi));
+  // (float storage: |w| < 2^52 so the f32 rounding cannot reach the 2^53
+  // integer limit; float64: exact below 2^53)
+  const double fast_limit = dtype == BTAS_I32 ? (double)kI32Limit : (dtype == BTAS_F32 ? 4503599627370496.0
+                                                                                       : 9007199254740992.0);
+  const bool fast = weights_mode != BTAS_WEIGHTS_UNIFORM &&
+                    !(weights_mode == BTAS_WEIGHTS_BOUNDED && range > (1ull << 53)) && mag < fast_limit;
+#define BTAS_FILL(T)                                                                                            \
+  (fast ? (fill_kernel<T, true><<<(unsigned)grid, kGenThreads, 0, st>>>(n, weights_mode, wide, low, draws,        \
+                                                                         static_cast<T*>(D), ld, w.bits, w.p_warp, \
+                                                                         w.p_base, w.p_ctas, stats_dev),           \
+           0)                                                                                                    \
+        : (fill_kernel<T, false><<<(unsigned)grid, kGenThreads, 0, st>>>(n, weights_mode, wide, low, draws,       \
+                                                                          static_cast<T*>(D), ld, w.bits,          \
+                                                                          w.p_warp, w.p_base, w.p_ctas, stats_dev), \
+           0))
   switch (dtype) {
     case BTAS_F32:
-      fill_kernel<float><<<(unsigned)grid, kGenThreads, 0, st>>>(n, weights_mode, wide, low, draws,
-                                                              static_cast<float*>(D), ld, w.bits, w.p_warp,
-                                                              w.p_base, w.p_ctas, stats_dev);
+      (void)BTAS_FILL(float);
       break;
     case BTAS_I32:
-      fill_kernel<int32_t><<<(unsigned)grid, kGenThreads, 0, st>>>(n, weights_mode, wide, low, draws,
-                                                              static_cast<int32_t*>(D), ld, w.bits, w.p_warp,
-                                                              w.p_base, w.p_ctas, stats_dev);
+      (void)BTAS_FILL(int32_t);
       break;
     case BTAS_F64:
-      fill_kernel<double><<<(unsigned)grid, kGenThreads, 0, st>>>(n, weights_mode, wide, low, draws,
-                                                              static_cast<double*>(D), ld, w.bits, w.p_warp,
-                                                              w.p_base, w.p_ctas, stats_dev);
+      (void)BTAS_FILL(double);
       break;
     default:
       return BTAS_ERR_INVALID;
   }
+#undef BTAS_FILL
   BTAS_CUDA_CHECK_LAUNCH();
   return BTAS_OK;
 }
