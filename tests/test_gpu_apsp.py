@@ -24,9 +24,15 @@ def digest(a):
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
-def test_golden_apsp_triple_equivalence(cuda, golden, dtype):
+@pytest.mark.parametrize("small_route", [True, False])
+def test_golden_apsp_triple_equivalence(cuda, golden, dtype, small_route, monkeypatch):
     """700 digraphs of test_acceptance.py:155-175: FW == squaring == the
-    reference, byte for byte, with the reference's multiplication counts."""
+    reference, byte for byte, with the reference's multiplication counts.
+    small_route=False disables the one-kernel small-graph squaring (and the
+    FW route through it), so the blocked FW and the btas_gemm loop are
+    checked on the same graphs."""
+    if not small_route:
+        monkeypatch.setenv("BTAS_APSP_SMALL_MAX_N", "0")
     g = golden("apsp_small.npz")
     meta = g["meta"]
     for case in range(len(meta)):
