@@ -267,8 +267,8 @@ __global__ void __launch_bounds__(kFw1Threads) fw_phase1_kernel(T* __restrict__ 
 }
 
 // ------------------------------------------------------------------ phase 2
-// blockIdx.y == 0: row panel (pivot rows x column block blockIdx.x), its own
-//                  row k each round, pivot-column snapshots fixed in smem
+// blockIdx.y == 0: row panel (pivot rows x column block blockIdx.x): own
+//                  operand = its row k each round, fixed = pivot-column snapshot
 // blockIdx.y == 1: column panel (row block blockIdx.x x pivot columns)
 // The fixed operand of every round (the pivot tile's column / row snapshot,
 // 64 KB, identical for all CTAs) is read through L1 one round ahead instead
