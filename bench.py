@@ -300,7 +300,10 @@ def main():
 
     # ------------------------------------------------------------- e2e (public API, host buffers)
     if not args.no_e2e:
-        e2e = e2e_gemm(n, dtype, xs, ys, dev, steps=max(3, args.steps))
+        try:
+            e2e = e2e_gemm(n, dtype, xs, ys, dev, steps=max(3, args.steps))
+        except (RuntimeError, MemoryError) as exc:  # e.g. pinned host memory exhausted: keep the line
+            e2e = {"error": f"{type(exc).__name__}: {exc}"[:300], "ms_per_step": float("nan")}
         if world > 1:  # whole job: every rank's steps over the slowest rank's time
             t = torch.tensor([e2e["ms_per_step"]], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
