@@ -153,16 +153,46 @@ BTAS_D void product(const SmallArgs<T>& a, const T* X, int64_t ldx, const T* Y, 
         pb[u] = (gk2 < n && gc < n) ? Y[gk2 * ldy + gc] : inf;
       }
     };
+    // f32 fast path: k-pair interleaved staging, so one 16-byte load gives a
+    // thread its two rows' (k, k+1) values and FADD2 + FMNMX3 form two
+    // candidates per add and per min (as in the GEMM kernel)
+    constexpr bool kPairs = Traits<T>::dtype == BTAS_F32 && !CHECKED;
+    float2(*A2)[kT + 2] = reinterpret_cast<float2(*)[kT + 2]>(&As[0][0]);  // [k/2][r] = (k even, k odd)
+    float2(*B2)[kT + 2] = reinterpret_cast<float2(*)[kT + 2]>(&Bs[0][0]);
     fetch(0);
     for (int64_t k0 = 0; k0 < n; k0 += kKC) {
 #pragma unroll
       for (int u = 0; u < kPer; ++u) {
         const int e = threadIdx.x + u * kThreads;
-        As[e % kKC][e / kKC] = pa[u];
-        Bs[e / kT][e % kT] = pb[u];
+        if constexpr (kPairs) {
+          const int k = e % kKC, r = e / kKC, kk = e / kT, c = e % kT;
+          reinterpret_cast<float*>(&A2[k >> 1][r])[k & 1] = pa[u];
+          reinterpret_cast<float*>(&B2[kk >> 1][c])[kk & 1] = pb[u];
+        } else {
+          As[e % kKC][e / kKC] = pa[u];
+          Bs[e / kT][e % kT] = pb[u];
+        }
       }
       __syncthreads();
       if (k0 + kKC < n) fetch(k0 + kKC);
+      if constexpr (kPairs) {
+#pragma unroll 8
+        for (int kp = 0; kp < kKC / 2; ++kp) {
+          const float4 xa = *reinterpret_cast<const float4*>(&A2[kp][ty * 2]);  // rows ty*2, ty*2+1
+          const float4 yb = *reinterpret_cast<const float4*>(&B2[kp][tx * 2]);  // cols tx*2, tx*2+1
+          const float2 x[2] = {make_float2(xa.x, xa.y), make_float2(xa.z, xa.w)};
+          const float2 y[2] = {make_float2(yb.x, yb.y), make_float2(yb.z, yb.w)};
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const float2 sum = __fadd2_rn(x[i], y[j]);
+              acc[i][j] = fminf(fminf(acc[i][j], sum.x), sum.y);
+            }
+        }
+        __syncthreads();
+        continue;
+      }
 #pragma unroll 8
       for (int k = 0; k < kKC; ++k) {
         T x0, x1, y0, y1;
