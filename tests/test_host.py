@@ -108,3 +108,23 @@ def test_public_names_cover_reference_hot_path():
     for name in hot:
         assert name in bt.__all__ and hasattr(bt, name), name
     assert issubclass(bt.DimensionMismatch, ValueError) and issubclass(bt.SemiringMismatch, ValueError)
+
+
+def test_bench_reference_arm_contract():
+    """bench.py --impl reference runs on the host alone and prints one JSON
+    line with the contract's keys (small n so the CPU suite stays fast)."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    res = subprocess.run([sys.executable, str(root / "bench.py"), "--impl", "reference", "--n", "512", "--steps", "1",
+                          "--warmup", "0"], capture_output=True, text=True, timeout=300, cwd=root)
+    assert res.returncode == 0, res.stderr[-2000:]
+    line = json.loads(res.stdout.strip().splitlines()[-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "higher_is_better", "impl", "cpu_baseline",
+                "e2e"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["e2e"]["h2d_bytes_per_step"] == 0
+    assert line["cpu_baseline"]["kind"] in ("port", "reference") and line["cpu_baseline"]["cores"] >= 1
