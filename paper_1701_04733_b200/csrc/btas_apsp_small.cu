@@ -361,10 +361,12 @@ int apsp_small_typed(int integer_mode, const T* base, int64_t ldb, int64_t n, T*
   a.steps = steps;
   a.result = result;
   a.flags = flags;
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apsp_small_kernel<T>, kThreads, 0) != cudaSuccess ||
-      per_sm < 1) {
+  static int per_sm = 0;  // per instantiation; the occupancy query costs tens of microseconds
+  if (per_sm < 1 &&
+      (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apsp_small_kernel<T>, kThreads, 0) != cudaSuccess ||
+       per_sm < 1)) {
     (void)cudaGetLastError();
+    per_sm = 0;
     return BTAS_ERR_CUDA;
   }
   const int64_t tiles = ceil_div(n, kT) * ceil_div(n, kT);
