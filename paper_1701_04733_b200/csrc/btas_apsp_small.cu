@@ -361,7 +361,9 @@ int apsp_small_typed(int integer_mode, const T* base, int64_t ldb, int64_t n, T*
   a.steps = steps;
   a.result = result;
   a.flags = flags;
-  static int per_sm = 0;  // per instantiation; the occupancy query costs tens of microseconds
+  // occupancy per instantiation (the query costs tens of microseconds; the
+  // kernel's resources, hence the answer, are the same on every B200)
+  static int per_sm = 0;
   if (per_sm < 1 &&
       (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apsp_small_kernel<T>, kThreads, 0) != cudaSuccess ||
        per_sm < 1)) {

@@ -132,6 +132,21 @@ BTAS_D void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t*
       : "memory");
 }
 
+// one bit per device: per-function attributes (dynamic shared memory limits)
+// are set once per device the process launches on
+inline bool configured_on_current_device(unsigned long long& mask) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  return dev < 64 && ((mask >> dev) & 1ull);
+}
+inline void mark_configured(unsigned long long& mask) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess && dev < 64) mask |= 1ull << dev;
+}
+
 BTAS_HD int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 BTAS_HD int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 

@@ -495,8 +495,8 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
 
   const size_t smem1 = 2 * (size_t)b * b * sizeof(T);
   const size_t smem2 = (size_t)b * b * sizeof(T);  // phase 2: the history array only
-  static bool configured = false;
-  if (!configured) {
+  static unsigned long long configured = 0;
+  if (!configured_on_current_device(configured)) {
     if (cudaFuncSetAttribute(fw_phase1_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem1) != cudaSuccess ||
         cudaFuncSetAttribute(fw_phase2_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -504,7 +504,7 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
       (void)cudaGetLastError();
       return BTAS_ERR_CUDA;
     }
-    configured = true;
+    mark_configured(configured);
   }
 
   // base GEMM descriptors over the full D; per launch only the k range
@@ -707,8 +707,8 @@ int fw_dist_stage_typed(int integer_mode, int stage, T* D, int64_t ld, int64_t n
   for (int q = 0; q < n_peers; ++q) f.peer_region[q] = static_cast<unsigned char*>(peers[q]);
   const size_t smem = 2 * (size_t)b * b * sizeof(T);
   const size_t smem2 = (size_t)b * b * sizeof(T);
-  static bool configured = false;
-  if (!configured) {
+  static unsigned long long configured = 0;
+  if (!configured_on_current_device(configured)) {
     if (cudaFuncSetAttribute(fw_phase1_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
             cudaSuccess ||
         cudaFuncSetAttribute(fw_phase2_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2) !=
@@ -716,7 +716,7 @@ int fw_dist_stage_typed(int integer_mode, int stage, T* D, int64_t ld, int64_t n
       (void)cudaGetLastError();
       return BTAS_ERR_CUDA;
     }
-    configured = true;
+    mark_configured(configured);
   }
   switch (stage) {
     case BTAS_FW_STAGE_INIT: {

@@ -586,14 +586,14 @@ int device_sm_count();
 template <class P, bool MIN, int EPI>
 int launch_gemm_epi(const GemmArgs& g, cudaStream_t stream) {
   using S = GemmShape<P>;
-  static bool configured = false;
-  if (!configured) {
+  static unsigned long long configured = 0;
+  if (!configured_on_current_device(configured)) {
     if (cudaFuncSetAttribute(tropical_gemm_kernel<P, MIN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)S::smem_bytes) != cudaSuccess) {
       (void)cudaGetLastError();
       return BTAS_ERR_CUDA;
     }
-    configured = true;
+    mark_configured(configured);
   }
   const int ntiles = g.mblocks * g.nblocks;
   const int grid = ntiles < device_sm_count() ? ntiles : device_sm_count();
