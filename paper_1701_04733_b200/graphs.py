@@ -29,6 +29,7 @@ import torch
 from . import _lib
 from .matrix import (
     TropicalMatrix,
+    _device_ctx,
     _dtype_code,
     _host_read,
     _kind_code,
@@ -117,6 +118,15 @@ def _weight_plan(low: float, high: float):
 def random_graph_matrix(n: int, p: float, weight_range, seed: int, *, dtype: "torch.dtype | None" = None,
                         device=None) -> TropicalMatrix:
     """The reference instance ``graph_to_matrix(random_graph(n, p, weight_range,
+    seed))`` generated on the GPU (see _random_graph_matrix)."""
+    dev = _resolve_device(device)
+    with _device_ctx(dev):
+        return _random_graph_matrix(n, p, weight_range, seed, dtype=dtype, device=dev)
+
+
+def _random_graph_matrix(n: int, p: float, weight_range, seed: int, *, dtype: "torch.dtype | None" = None,
+                         device=None) -> TropicalMatrix:
+    """The reference instance ``graph_to_matrix(random_graph(n, p, weight_range,
     seed))`` generated on the GPU (include/btas_cuda.h btas_graph_*): presence
     draws, weight draws and the dense fill run as CUDA kernels over the same
     PCG64 stream, so the matrix is bit-identical to the reference's (and to
@@ -190,6 +200,15 @@ def random_graph_matrix_host(n: int, p: float, weight_range, seed: int, *, dtype
 
 
 def edges_to_matrix(n: int, src, dst, weight, *, dtype: "torch.dtype | None" = None, device=None) -> TropicalMatrix:
+    """graph_to_matrix of an edge list; see _edges_to_matrix."""
+    if not isinstance(n, int) or n < 1:
+        raise ValueError(f"vertex count must be a positive integer, got {n!r}")
+    dev = _resolve_device(device)
+    with _device_ctx(dev):
+        return _edges_to_matrix(n, src, dst, weight, dtype=dtype, device=dev)
+
+
+def _edges_to_matrix(n: int, src, dst, weight, *, dtype: "torch.dtype | None" = None, device=None) -> TropicalMatrix:
     """``graph_to_matrix`` (graph_io.py:158-165) of an edge list given as three
     equal-length arrays (numpy or torch; src/dst integer, weight float):
     +inf off the diagonal, 0 on it, duplicates keep the minimum weight and a

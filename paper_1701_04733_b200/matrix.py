@@ -124,6 +124,35 @@ def _resolve_device(device) -> torch.device:
     return dev
 
 
+def _on_operand_device(fn):
+    """Run ``fn`` with the CUDA device of its first matrix/vector/tensor
+    argument current, so its kernels launch on the operands' device even when
+    one process drives several GPUs (one process per GPU needs nothing)."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(*args, **kwargs):
+        for a in args:
+            t = a.data if hasattr(a, "data") and isinstance(getattr(a, "data"), torch.Tensor) else a
+            if isinstance(t, torch.Tensor) and t.is_cuda:
+                if t.device.index == torch.cuda.current_device():
+                    return fn(*args, **kwargs)
+                with torch.cuda.device(t.device):
+                    return fn(*args, **kwargs)
+        return fn(*args, **kwargs)
+
+    return wrapper
+
+
+def _device_ctx(device: torch.device):
+    """Context making ``device`` current for the kernels a call launches."""
+    import contextlib
+
+    if device.type != "cuda" or device.index == torch.cuda.current_device():
+        return contextlib.nullcontext()
+    return torch.cuda.device(device)
+
+
 def _stream(device: torch.device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
@@ -266,6 +295,11 @@ def _new_stats(device: torch.device) -> torch.Tensor:
 
 
 def _ingest(kind: SemiringKind, values, dtype: torch.dtype, device: torch.device, ndim: int):
+    with _device_ctx(device):
+        return _ingest_on_device(kind, values, dtype, device, ndim)
+
+
+def _ingest_on_device(kind: SemiringKind, values, dtype: torch.dtype, device: torch.device, ndim: int):
     """Validate symbolic-form input and produce oriented device storage.
 
     Mirrors _orient/_detect_integer (reference matrix.py:82-115) on the GPU:
@@ -542,7 +576,8 @@ def identity_matrix(kind: SemiringKind, n: int, *, dtype: "torch.dtype | None" =
     dt = dtype if dtype is not None else _default_dtype
     dev = _resolve_device(device)
     data = torch.empty((n, n), dtype=dt, device=dev)
-    _lib.call("btas_identity", _dtype_code(dt), _kind_code(kind), _ptr(data), n, n, _stream(dev))
+    with _device_ctx(dev):
+        _lib.call("btas_identity", _dtype_code(dt), _kind_code(kind), _ptr(data), n, n, _stream(dev))
     return TropicalMatrix._wrap(kind, data, True)
 
 
@@ -558,6 +593,7 @@ def _check_same_storage(a, b) -> None:
         raise ValueError(f"operands live on different devices: {a.device} vs {b.device}")
 
 
+@_on_operand_device
 def ew_add(a, b):
     """Elementwise ⊕ (reference matrix.py:271-277), for matrices and vectors.
 
@@ -621,6 +657,7 @@ def _rowmajor(t: torch.Tensor) -> torch.Tensor:
     return t if t.stride(1) == 1 else t.contiguous()
 
 
+@_on_operand_device
 def matmul(x: TropicalMatrix, y: TropicalMatrix, accumulate_into: "TropicalMatrix | None" = None,
            tiles: "TileSpec | None" = None) -> TropicalMatrix:
     """Tropical product, optionally fused with an elementwise ⊕.
@@ -652,6 +689,7 @@ def matmul(x: TropicalMatrix, y: TropicalMatrix, accumulate_into: "TropicalMatri
     return TropicalMatrix._wrap(x.kind, out, integer)
 
 
+@_on_operand_device
 def matvec(a: TropicalMatrix, v: TropicalVector) -> TropicalVector:
     """out(i) = ⊕_k a(i,k) ⊗ v(k) (reference matrix.py:403-425)."""
     _check_same_kind(a, v)
@@ -662,6 +700,7 @@ def matvec(a: TropicalMatrix, v: TropicalVector) -> TropicalVector:
     return TropicalVector._wrap(a.kind, out.reshape(-1), a.integer and v.integer)
 
 
+@_on_operand_device
 def matvec_batched(a: TropicalMatrix, vs: "torch.Tensor | TropicalMatrix", integer: "bool | None" = None) -> torch.Tensor:
     """Batched matvec: rows of ``vs`` (B x K, oriented storage of a's dtype)
     are B vectors; returns the B x M oriented results (one HBM pass over A
@@ -691,6 +730,7 @@ def matvec_batched(a: TropicalMatrix, vs: "torch.Tensor | TropicalMatrix", integ
     return out
 
 
+@_on_operand_device
 def matrix_power(a: TropicalMatrix, p: int, tiles: "TileSpec | None" = None) -> TropicalMatrix:
     """Semiring p-th power by LSB-first binary exponentiation
     (reference matrix.py:428-448); ``matrix_power(a, 1) is a``."""
