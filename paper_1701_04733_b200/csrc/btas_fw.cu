@@ -542,25 +542,50 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
   // one phase-3 style update over K = halves * b (pivot-block slots
   // [0, halves) of the panels): 32-bit kernel gated on "s16 overflow",
   // s16x2 kernel gated on "no overflow"
-  auto phase3 = [&](GemmArgs a, GemmArgs a16, int halves) -> int {
+  auto phase3_on = [&](GemmArgs a, GemmArgs a16, int halves, cudaStream_t s) -> int {
     a.Kp2 = (int64_t)halves * b / 2;
     a16.Kp2 = (int64_t)halves * b / 4;
     a.gate = emit_s16 ? &ctrl->s16_overflow[0] : nullptr;
     a16.gate = &ctrl->s16_overflow[0];
     int rc;
     if constexpr (CHECKED) {
-      rc = launch_gemm_epi<MixChecked<T, true>, true, kEpiAcc>(a, st);
+      rc = launch_gemm_epi<MixChecked<T, true>, true, kEpiAcc>(a, s);
     } else if constexpr (Traits<T>::dtype == BTAS_F64) {
-      rc = launch_gemm_epi<MixF64<true>, true, kEpiAcc>(a, st);
+      rc = launch_gemm_epi<MixF64<true>, true, kEpiAcc>(a, s);
     } else if constexpr (Traits<T>::dtype == BTAS_I32) {
-      rc = launch_gemm_epi<MixI32<true>, true, kEpiAcc>(a, st);
+      rc = launch_gemm_epi<MixI32<true>, true, kEpiAcc>(a, s);
     } else {
-      rc = launch_gemm_epi<MixF32<true>, true, kEpiAcc>(a, st);
+      rc = launch_gemm_epi<MixF32<true>, true, kEpiAcc>(a, s);
     }
     if (rc) return rc;
-    if (emit_s16) rc = launch_gemm_epi<MixS16<true, T>, true, kEpiAcc>(a16, st);
+    if (emit_s16) rc = launch_gemm_epi<MixS16<true, T>, true, kEpiAcc>(a16, s);
     return rc;
   };
+  auto phase3 = [&](GemmArgs a, GemmArgs a16, int halves) -> int { return phase3_on(a, a16, halves, st); };
+  // The row- and column-panel thin passes of a pivot block touch disjoint
+  // tiles and each fills only n/128 CTAs: the column pass runs on a side
+  // stream, forked from and joined back into the caller's stream (per host
+  // thread and device, created once), so both share the SMs.
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  {
+    thread_local cudaStream_t t_side[64] = {};
+    thread_local cudaEvent_t t_fork[64] = {}, t_join[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && dev < 64) {
+      if (!t_side[dev] && (cudaStreamCreateWithFlags(&t_side[dev], cudaStreamNonBlocking) != cudaSuccess ||
+                           cudaEventCreateWithFlags(&t_fork[dev], cudaEventDisableTiming) != cudaSuccess ||
+                           cudaEventCreateWithFlags(&t_join[dev], cudaEventDisableTiming) != cudaSuccess)) {
+        (void)cudaGetLastError();
+        t_side[dev] = nullptr;
+      }
+      side = t_side[dev];
+      fork_ev = t_fork[dev];
+      join_ev = t_join[dev];
+    } else {
+      (void)cudaGetLastError();
+    }
+  }
   auto phases12 = [&](int kb, int slot) -> int {
     f.k0 = (int64_t)kb * b;
     f.koff = slot * b;
@@ -588,6 +613,10 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
       const int kb = kb0 + j;
       const int64_t kk = (int64_t)kb * b, mk = std::min<int64_t>(b, n - kk);
       if (j > 0) {
+        const bool fork = side != nullptr;
+        if (fork &&
+            (cudaEventRecord(fork_ev, st) != cudaSuccess || cudaStreamWaitEvent(side, fork_ev, 0) != cudaSuccess))
+          return BTAS_ERR_CUDA;
         {  // pending updates -> row block kb
           GemmArgs a = g, a16 = g16;
           a.M = a16.M = mk;
@@ -598,7 +627,7 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
           a.Z = a16.Z = D + kk * ld;
           if ((rc = phase3(a, a16, j))) return rc;
         }
-        {  // pending updates -> column block kb (its rows in block kb just done)
+        {  // pending updates -> column block kb outside the pivot rows (disjoint from the row pass)
           GemmArgs a = g, a16 = g16;
           a.N = a16.N = mk;
           a.nblocks = a16.nblocks = 1;
@@ -608,8 +637,11 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
           a.Z = a16.Z = D + kk;
           a.skip_row_lo = a16.skip_row_lo = kk;
           a.skip_row_hi = a16.skip_row_hi = kk + b;
-          if ((rc = phase3(a, a16, j))) return rc;
+          if ((rc = phase3_on(a, a16, j, fork ? side : st))) return rc;
         }
+        if (fork &&
+            (cudaEventRecord(join_ev, side) != cudaSuccess || cudaStreamWaitEvent(st, join_ev, 0) != cudaSuccess))
+          return BTAS_ERR_CUDA;
       }
       if ((rc = phases12(kb, j))) return rc;
     }
