@@ -3,6 +3,7 @@
 // All are grid-stride, 16-byte vectorised where alignment allows, and sized
 // to a multiple of the SM count.
 #include <algorithm>
+#include <cuda.h>
 #include <type_traits>
 
 #include "btas_common.cuh"
@@ -330,23 +331,27 @@ __global__ void __launch_bounds__(256) matvec_kernel(const T* __restrict__ A, in
 // ---- many vectors (5-8) of 4-byte storage: one pass over A -----------------
 // With 8 vectors every A element feeds 8 add-min pairs, so the pass is only
 // HBM-bound if A streams with enough bytes in flight AND the vectors are not
-// re-read from L2 for every few rows.  CTA = 32 rows (warp w: rows 4w..4w+3);
-// per 256-column chunk each lane streams 4 rows x 2 float4 of A into
-// registers (two CTAs per SM) while the chunk's 8 vector slices (8 KB) sit in
-// shared memory, double-buffered with cp.async, so L2 sees each vector once
-// per 32 rows.  The pass is issue-bound (8 add-min pairs per A element), so
-// the finite-magnitude screen costs two integer ops per element (abs_key).  The exact overflow screen is the
-// one of matvec_kernel; a CTA whose screen fails recomputes its rows with the
-// masked candidates.
-constexpr int kWideRows = 32, kWideChunk = 256, kWideNB = 8, kWideThreads = 256;
+// re-read from L2 for every few rows.  CTA = 32 rows (warp w: rows 4w..4w+3),
+// two CTAs per SM.  Per 128-column chunk one producer thread issues two 2-D
+// tensor-map TMA copies (the 32 x 128 A tile and the 8 x 128 vector tile)
+// into a 4-stage shared-memory ring with full/empty mbarriers, so three
+// chunks per CTA are in flight while the warps compute on the fourth,
+// without registers or issue slots spent on the loads.  The
+// finite-magnitude screen costs two integer ops per element (abs_key).  The
+// exact overflow screen is the one of matvec_kernel; a CTA whose screen
+// fails recomputes its rows with the masked candidates.
+constexpr int kWideRows = 32, kWideChunk = 128, kWideNB = 8, kWideThreads = 256, kWideStages = 4;
+// one stage: the CTA's 32 x 128 tile of A, then the 8 x 128 vector tile
+constexpr int kWideStageElems = (kWideRows + kWideNB) * kWideChunk;
+constexpr uint32_t kWideStageBytes = kWideStageElems * 4;
+constexpr size_t kWideSmem = (size_t)kWideStages * kWideStageBytes + 2 * kWideStages * sizeof(uint64_t);
 
-BTAS_D void cp_async16(void* smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
-}
-BTAS_D void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-BTAS_D void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+BTAS_D void tma_2d(void* smem_dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
 }
 
 // max |finite| bookkeeping in one or two integer ops per element: the
@@ -365,96 +370,94 @@ BTAS_D T key_abs(int32_t k) {
 }
 
 template <class T, bool MIN>
-__global__ void __launch_bounds__(kWideThreads, 2) matvec_wide_kernel(const T* __restrict__ A, int64_t lda, int64_t M,
+__global__ void __launch_bounds__(kWideThreads, 2) matvec_wide_kernel(const __grid_constant__ CUtensorMap mapA,
+                                                                   const __grid_constant__ CUtensorMap mapV,
+                                                                   const T* __restrict__ A, int64_t lda, int64_t M,
                                                                    int64_t K, const T* __restrict__ Vv, int64_t ldv,
                                                                    int nb, T* __restrict__ Out, int64_t ldo,
                                                                    int int_mode, double limit, int32_t* flags) {
   static_assert(sizeof(T) == 4, "4-byte storage");
-  __shared__ __align__(16) T Vs[2][kWideNB][kWideChunk];
+  extern __shared__ __align__(128) unsigned char wide_smem[];
+  T* stages = reinterpret_cast<T*>(wide_smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(wide_smem + (size_t)kWideStages * kWideStageBytes);
+  uint64_t* empty = full + kWideStages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r0 = (int64_t)blockIdx.x * kWideRows;
   const T eps = Traits<T>::eps(MIN);
   const int64_t nchunks = K / kWideChunk;  // the caller guarantees K % kWideChunk == 0
-  // stage vector chunk c into buffer c & 1 (vectors past nb are eps)
-  auto stage = [&](int64_t c) {
-    T(*dst)[kWideChunk] = Vs[c & 1];
-    for (int e = threadIdx.x; e < kWideNB * kWideChunk / 4; e += kWideThreads) {
-      const int b = e / (kWideChunk / 4), q = e % (kWideChunk / 4);
-      if (b < nb) {
-        cp_async16(&dst[b][q * 4], Vv + (int64_t)b * ldv + c * kWideChunk + q * 4);
-      } else {
-        T* d = &dst[b][q * 4];
-        d[0] = d[1] = d[2] = d[3] = eps;
-      }
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kWideStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], kWideThreads / 32);
     }
-    cp_async_commit();
+    fence_mbar_init();
+  }
+  __syncthreads();
+  // thread 0 is the producer: two tensor-map copies per stage (rows past M
+  // and vectors past nb arrive zero-filled; their results are never stored)
+  auto issue = [&](int64_t c) {
+    const int st = (int)(c % kWideStages);
+    T* dst = stages + (size_t)st * kWideStageElems;
+    mbar_arrive_expect_tx(&full[st], kWideStageBytes);
+    tma_2d(dst, &mapA, (int)(c * kWideChunk), (int)r0, &full[st]);
+    tma_2d(dst + kWideRows * kWideChunk, &mapV, (int)(c * kWideChunk), 0, &full[st]);
   };
+  if (threadIdx.x == 0)
+    for (int64_t c = 0; c < nchunks && c < kWideStages; ++c) issue(c);
   T acc[4][kWideNB];
 #pragma unroll
   for (int r = 0; r < 4; ++r)
 #pragma unroll
     for (int b = 0; b < kWideNB; ++b) acc[r][b] = eps;
   int32_t akey = 0, vkey = 0;
-  const T* arow[4];
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int64_t row = r0 + warp * 4 + r;
-    arow[r] = A + (row < M ? row : M - 1) * lda;
-  }
-  stage(0);
   for (int64_t c = 0; c < nchunks; ++c) {
-    uint4 av[4][kWideChunk / 128];
+    const int st = (int)(c % kWideStages);
+    const uint32_t use = (uint32_t)((c / kWideStages) & 1);
+    mbar_wait(&full[st], use);
+    const T* src = stages + (size_t)st * kWideStageElems;
+    const int col = lane * 4;
+    T v[kWideNB][4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int b = 0; b < kWideNB; ++b) {
+      const uint4 u = *reinterpret_cast<const uint4*>(&src[(kWideRows + b) * kWideChunk + col]);
+      v[b][0] = __builtin_bit_cast(T, u.x);
+      v[b][1] = __builtin_bit_cast(T, u.y);
+      v[b][2] = __builtin_bit_cast(T, u.z);
+      v[b][3] = __builtin_bit_cast(T, u.w);
+      if (warp == 0 && b < nb) {
 #pragma unroll
-      for (int j = 0; j < kWideChunk / 128; ++j)
-        av[r][j] = __ldcs(reinterpret_cast<const uint4*>(arow[r] + c * kWideChunk + j * 128 + lane * 4));
-    if (c + 1 < nchunks) {
-      stage(c + 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
+        for (int e = 0; e < 4; ++e) vkey = max(vkey, abs_key(v[b][e]));
+      }
     }
-    __syncthreads();
-    const T(*vs)[kWideChunk] = Vs[c & 1];
+    uint4 au[4];
 #pragma unroll
-    for (int j = 0; j < kWideChunk / 128; ++j) {
-      const int col = j * 128 + lane * 4;
-      T v[kWideNB][4];
+    for (int r = 0; r < 4; ++r) au[r] = *reinterpret_cast<const uint4*>(&src[(warp * 4 + r) * kWideChunk + col]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);  // this warp's reads of the stage are done
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const T a[4] = {__builtin_bit_cast(T, au[r].x), __builtin_bit_cast(T, au[r].y), __builtin_bit_cast(T, au[r].z),
+                      __builtin_bit_cast(T, au[r].w)};
+      akey = max(akey, max(max(abs_key(a[0]), abs_key(a[1])), max(abs_key(a[2]), abs_key(a[3]))));
 #pragma unroll
       for (int b = 0; b < kWideNB; ++b) {
-        const uint4 u = *reinterpret_cast<const uint4*>(&vs[b][col]);
-        v[b][0] = __builtin_bit_cast(T, u.x);
-        v[b][1] = __builtin_bit_cast(T, u.y);
-        v[b][2] = __builtin_bit_cast(T, u.z);
-        v[b][3] = __builtin_bit_cast(T, u.w);
-        if (warp == 0) {
+        if constexpr (Traits<T>::dtype == BTAS_F32) {
 #pragma unroll
-          for (int e = 0; e < 4; ++e) vkey = max(vkey, abs_key(v[b][e]));
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const T a[4] = {__builtin_bit_cast(T, av[r][j].x), __builtin_bit_cast(T, av[r][j].y),
-                        __builtin_bit_cast(T, av[r][j].z), __builtin_bit_cast(T, av[r][j].w)};
-        akey = max(akey, max(max(abs_key(a[0]), abs_key(a[1])), max(abs_key(a[2]), abs_key(a[3]))));
-#pragma unroll
-        for (int b = 0; b < kWideNB; ++b) {
-          if constexpr (Traits<T>::dtype == BTAS_F32) {
-#pragma unroll
-            for (int e = 0; e < 4; e += 2) {
-              const float2 s2 = __fadd2_rn(make_float2(a[e], a[e + 1]), make_float2(v[b][e], v[b][e + 1]));
-              acc[r][b] = MIN ? fminf(fminf(acc[r][b], s2.x), s2.y) : fmaxf(fmaxf(acc[r][b], s2.x), s2.y);
-            }
-          } else {
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              acc[r][b] = MIN ? __viaddmin_s32(a[e], v[b][e], acc[r][b]) : __viaddmax_s32(a[e], v[b][e], acc[r][b]);
+          for (int e = 0; e < 4; e += 2) {
+            const float2 s2 = __fadd2_rn(make_float2(a[e], a[e + 1]), make_float2(v[b][e], v[b][e + 1]));
+            acc[r][b] = MIN ? fminf(fminf(acc[r][b], s2.x), s2.y) : fmaxf(fmaxf(acc[r][b], s2.x), s2.y);
           }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            acc[r][b] = MIN ? __viaddmin_s32(a[e], v[b][e], acc[r][b]) : __viaddmax_s32(a[e], v[b][e], acc[r][b]);
         }
       }
     }
-    __syncthreads();  // buffer c & 1 is restaged at iteration c + 1
+    if (threadIdx.x == 0 && c + kWideStages < nchunks) {
+      mbar_wait(&empty[st], use);  // every warp has read stage st: refill it
+      issue(c + kWideStages);
+    }
   }
   T amax = key_abs<T>(akey), vmax = key_abs<T>(vkey);
   // exact screen over the CTA (see matvec_kernel)
@@ -532,6 +535,39 @@ __global__ void __launch_bounds__(kWideThreads, 2) matvec_wide_kernel(const T* _
   if (__any_sync(0xffffffffu, sat) && lane == 0) atomicOr(&flags[BTAS_FLAG_SATURATED], 1);
 }
 
+// 2-D tensor maps for matvec_wide_kernel (cuTensorMapEncodeTiled through the
+// runtime's driver entry point: no link-time libcuda dependency)
+using TensorMapEncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                       const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                       CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+inline TensorMapEncodeFn tensor_map_encoder() {
+  static const TensorMapEncodeFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      (void)cudaGetLastError();
+      p = nullptr;
+    }
+    return reinterpret_cast<TensorMapEncodeFn>(p);
+  }();
+  return fn;
+}
+// rows x cols row-major 4-byte matrix with leading dimension ld; box of
+// kWideChunk columns x box_rows rows; out-of-range rows read as zero
+inline bool wide_tensor_map(CUtensorMap* m, bool f32, const void* base, int64_t rows, int64_t cols, int64_t ld,
+                            int box_rows) {
+  const TensorMapEncodeFn enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)kWideChunk, (cuuint32_t)box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  return enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_INT32, 2, const_cast<void*>(base), dims,
+             strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <class T, bool MIN>
 int matvec_typed(int int_mode, const T* A, int64_t lda, int64_t M, int64_t K, const T* V, int64_t ldv,
                  int64_t batch, T* Out, int64_t ldo, int32_t* flags, cudaStream_t st) {
@@ -549,10 +585,21 @@ int matvec_typed(int int_mode, const T* A, int64_t lda, int64_t M, int64_t K, co
     b0 += nb;
     if constexpr (sizeof(T) == 4) {
       if (nb > 4) {
-        matvec_wide_kernel<T, MIN><<<(unsigned)ceil_div(M, kWideRows), kWideThreads, 0, st>>>(A, lda, M, K, Vb,
-                                                                                                  ldv, nb,
-                                                                                         Ob, ldo, int_mode, limit,
-                                                                                         flags);
+        CUtensorMap mapA, mapV;
+        if (!wide_tensor_map(&mapA, Traits<T>::dtype == BTAS_F32, A, M, K, lda, kWideRows) ||
+            !wide_tensor_map(&mapV, Traits<T>::dtype == BTAS_F32, Vb, nb, K, ldv, kWideNB))
+          return BTAS_ERR_CUDA;
+        static unsigned long long configured = 0;
+        if (!configured_on_current_device(configured)) {
+          if (cudaFuncSetAttribute(matvec_wide_kernel<T, MIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)kWideSmem) != cudaSuccess) {
+            (void)cudaGetLastError();
+            return BTAS_ERR_CUDA;
+          }
+          mark_configured(configured);
+        }
+        matvec_wide_kernel<T, MIN><<<(unsigned)ceil_div(M, kWideRows), kWideThreads, kWideSmem, st>>>(
+            mapA, mapV, A, lda, M, K, Vb, ldv, nb, Ob, ldo, int_mode, limit, flags);
         BTAS_CUDA_CHECK_LAUNCH();
         continue;
       }
