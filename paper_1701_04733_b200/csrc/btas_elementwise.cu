@@ -332,16 +332,17 @@ __global__ void __launch_bounds__(256) matvec_kernel(const T* __restrict__ A, in
 // With 8 vectors every A element feeds 8 add-min pairs, so the pass is only
 // HBM-bound if A streams with enough bytes in flight AND the vectors are not
 // re-read from L2 for every few rows.  CTA = 32 rows (warp w: rows 4w..4w+3),
-// two CTAs per SM.  Per 128-column chunk one producer thread issues two 2-D
-// tensor-map TMA copies (the 32 x 128 A tile and the 8 x 128 vector tile)
-// into a 4-stage shared-memory ring with full/empty mbarriers, so three
-// chunks per CTA are in flight while the warps compute on the fourth,
+// two CTAs per SM.  Per 256-column chunk one producer thread issues two 2-D
+// tensor-map TMA copies (the 32 x 256 A tile and the 8 x 256 vector tile)
+// into a 2-stage shared-memory ring (40 KB per stage) with full/empty
+// mbarriers, so the next chunk is in flight while the warps compute,
 // without registers or issue slots spent on the loads.  The
 // finite-magnitude screen costs two integer ops per element (abs_key).  The
 // exact overflow screen is the one of matvec_kernel; a CTA whose screen
 // fails recomputes its rows with the masked candidates.
-constexpr int kWideRows = 32, kWideChunk = 128, kWideNB = 8, kWideThreads = 256, kWideStages = 4;
+constexpr int kWideRows = 32, kWideChunk = 256, kWideNB = 8, kWideThreads = 256, kWideStages = 2;
 // one stage: the CTA's 32 x 128 tile of A, then the 8 x 128 vector tile
+static_assert(kWideChunk % 128 == 0 && kWideChunk <= 256, "a warp covers 128 columns per step; TMA box <= 256");
 constexpr int kWideStageElems = (kWideRows + kWideNB) * kWideChunk;
 constexpr uint32_t kWideStageBytes = kWideStageElems * 4;
 constexpr size_t kWideSmem = (size_t)kWideStages * kWideStageBytes + 2 * kWideStages * sizeof(uint64_t);
@@ -415,42 +416,47 @@ __global__ void __launch_bounds__(kWideThreads, 2) matvec_wide_kernel(const __gr
     const uint32_t use = (uint32_t)((c / kWideStages) & 1);
     mbar_wait(&full[st], use);
     const T* src = stages + (size_t)st * kWideStageElems;
-    const int col = lane * 4;
-    T v[kWideNB][4];
 #pragma unroll
-    for (int b = 0; b < kWideNB; ++b) {
-      const uint4 u = *reinterpret_cast<const uint4*>(&src[(kWideRows + b) * kWideChunk + col]);
-      v[b][0] = __builtin_bit_cast(T, u.x);
-      v[b][1] = __builtin_bit_cast(T, u.y);
-      v[b][2] = __builtin_bit_cast(T, u.z);
-      v[b][3] = __builtin_bit_cast(T, u.w);
-      if (warp == 0 && b < nb) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) vkey = max(vkey, abs_key(v[b][e]));
-      }
-    }
-    uint4 au[4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) au[r] = *reinterpret_cast<const uint4*>(&src[(warp * 4 + r) * kWideChunk + col]);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);  // this warp's reads of the stage are done
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const T a[4] = {__builtin_bit_cast(T, au[r].x), __builtin_bit_cast(T, au[r].y), __builtin_bit_cast(T, au[r].z),
-                      __builtin_bit_cast(T, au[r].w)};
-      akey = max(akey, max(max(abs_key(a[0]), abs_key(a[1])), max(abs_key(a[2]), abs_key(a[3]))));
+    for (int j = 0; j < kWideChunk / 128; ++j) {
+      const int col = j * 128 + lane * 4;
+      T v[kWideNB][4];
 #pragma unroll
       for (int b = 0; b < kWideNB; ++b) {
-        if constexpr (Traits<T>::dtype == BTAS_F32) {
+        const uint4 u = *reinterpret_cast<const uint4*>(&src[(kWideRows + b) * kWideChunk + col]);
+        v[b][0] = __builtin_bit_cast(T, u.x);
+        v[b][1] = __builtin_bit_cast(T, u.y);
+        v[b][2] = __builtin_bit_cast(T, u.z);
+        v[b][3] = __builtin_bit_cast(T, u.w);
+        if (warp == 0 && b < nb) {
 #pragma unroll
-          for (int e = 0; e < 4; e += 2) {
-            const float2 s2 = __fadd2_rn(make_float2(a[e], a[e + 1]), make_float2(v[b][e], v[b][e + 1]));
-            acc[r][b] = MIN ? fminf(fminf(acc[r][b], s2.x), s2.y) : fmaxf(fmaxf(acc[r][b], s2.x), s2.y);
+          for (int e = 0; e < 4; ++e) vkey = max(vkey, abs_key(v[b][e]));
+        }
+      }
+      uint4 au[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) au[r] = *reinterpret_cast<const uint4*>(&src[(warp * 4 + r) * kWideChunk + col]);
+      if (j == kWideChunk / 128 - 1) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);  // this warp's reads of the stage are done
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const T a[4] = {__builtin_bit_cast(T, au[r].x), __builtin_bit_cast(T, au[r].y), __builtin_bit_cast(T, au[r].z),
+                        __builtin_bit_cast(T, au[r].w)};
+        akey = max(akey, max(max(abs_key(a[0]), abs_key(a[1])), max(abs_key(a[2]), abs_key(a[3]))));
+#pragma unroll
+        for (int b = 0; b < kWideNB; ++b) {
+          if constexpr (Traits<T>::dtype == BTAS_F32) {
+#pragma unroll
+            for (int e = 0; e < 4; e += 2) {
+              const float2 s2 = __fadd2_rn(make_float2(a[e], a[e + 1]), make_float2(v[b][e], v[b][e + 1]));
+              acc[r][b] = MIN ? fminf(fminf(acc[r][b], s2.x), s2.y) : fmaxf(fmaxf(acc[r][b], s2.x), s2.y);
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              acc[r][b] = MIN ? __viaddmin_s32(a[e], v[b][e], acc[r][b]) : __viaddmax_s32(a[e], v[b][e], acc[r][b]);
           }
-        } else {
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            acc[r][b] = MIN ? __viaddmin_s32(a[e], v[b][e], acc[r][b]) : __viaddmax_s32(a[e], v[b][e], acc[r][b]);
         }
       }
     }
