@@ -36,7 +36,7 @@ def test_matvec_batched_large(cuda, dtype):
         asym = rand_sym(rng, m, k, -1000, 1000, p_inf=0.1)
         for kind in (MIN, MAX):
             a = bt.TropicalMatrix(kind, asym, dtype=dtype)
-            for batch in (1, 3, 8, 11):
+            for batch in (1, 3, 6, 8, 11):
                 vs = rand_sym(rng, batch, k, -1000, 1000, p_inf=0.1)
                 V = bt.TropicalMatrix(kind, vs, dtype=dtype)
                 out = bm._to_f64(bt.matvec_batched(a, V)).cpu().numpy()
