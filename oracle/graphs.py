@@ -54,3 +54,121 @@ def random_graph_dense(n: int, p: float, weight_range, seed: int) -> np.ndarray:
     mask = ~np.eye(n, dtype=bool)
     arr[mask] = off  # row-major over the off-diagonal pairs
     return arr
+
+
+# ---------------------------------------------------------------------------
+# row blocks of very large instances (n = 65536: n(n-1) = 4.3e9 presence
+# doubles, ~2.1e9 weight draws) without walking the streams on one core
+# ---------------------------------------------------------------------------
+_SEG = 1 << 22  # stream units per worker task
+
+
+def _threads(threads):
+    import os
+
+    return threads or len(os.sched_getaffinity(0))
+
+
+def _count_present(seed: int, start: int, stop: int, p: float, threads=None) -> int:
+    """#{t in [start, stop): presence double t < p} over the reference's
+    presence stream (one ``Generator.random()`` double per ordered pair,
+    graph_io.py:296-298), counted in parallel from PCG64.advance'd copies.
+    numpy's own ``random()`` produces the doubles."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    def seg(s0):
+        bg = np.random.PCG64(seed)
+        bg.advance(s0)
+        g = np.random.Generator(bg)
+        m = min(_SEG, stop - s0)
+        return int(np.count_nonzero(g.random(m) < p))
+
+    with ThreadPoolExecutor(_threads(threads)) as ex:
+        return sum(ex.map(seg, range(start, stop, _SEG)))
+
+
+def _lemire32_accept(raw: np.ndarray, rng: int) -> np.ndarray:
+    """Accepted mask of numpy's buffered bounded Lemire draw (numpy 2.3.5
+    ``random_buffered_bounded_lemire_uint32``, the path of
+    ``Generator.integers(low, high + 1)`` for ranges below 2^32 - 1) over the
+    32-bit words of raw 64-bit outputs, low half first (numpy's
+    ``next_uint32`` buffering).  A word is rejected iff the low 32 bits of
+    word * (rng + 1) fall below (2^32 - (rng + 1)) mod (rng + 1); acceptance
+    is per word, so counts over disjoint segments add up."""
+    words = raw.view(np.uint32).astype(np.uint64)  # little-endian: low half first
+    excl = np.uint64(rng + 1)
+    thresh = np.uint64(((1 << 32) - (rng + 1)) % (rng + 1))
+    return ((words * excl) & np.uint64(0xFFFFFFFF)) >= thresh
+
+
+def _locate_draw(seed: int, wstart: int, index: int, rng: int, threads=None) -> "tuple[int, int]":
+    """(64-bit unit, half) of the weight stream holding accepted draw number
+    ``index`` (0-based) of the stream that starts at unit ``wstart``."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    def count(s0):
+        bg = np.random.PCG64(seed)
+        bg.advance(s0)
+        return int(np.count_nonzero(_lemire32_accept(bg.random_raw(_SEG), rng)))
+
+    # accepted draws per unit are ~2, so index/2 units suffice, plus slack
+    nthr = _threads(threads)
+    base, need = wstart, index
+    with ThreadPoolExecutor(nthr) as ex:
+        while True:
+            starts = [base + i * _SEG for i in range(nthr)]
+            counts = list(ex.map(count, starts))
+            for s0, c in zip(starts, counts):
+                if need < c:
+                    bg = np.random.PCG64(seed)
+                    bg.advance(s0)
+                    acc = np.flatnonzero(_lemire32_accept(bg.random_raw(_SEG), rng))
+                    w = int(acc[need])
+                    return s0 + w // 2, w % 2
+                need -= c
+            base = starts[-1] + _SEG
+
+
+def instance_rows(n: int, p: float, weight_range, seed: int, r0: int, r1: int, threads=None) -> np.ndarray:
+    """Rows [r0, r1) of graph_to_matrix(random_graph(n, p, weight_range,
+    seed)) (graph_io.py:273-304, 158-165) for integer weight ranges, without
+    generating the rows before r0 one by one: the presence doubles before the
+    block are counted in parallel, the weight stream is positioned at the
+    first draw of the block, and numpy's own Generator then produces the
+    block's presence doubles and weights.  Symbolic float64 rows (diagonal 0,
+    absent +inf); equals the same rows of ``random_graph_dense``."""
+    low, high = float(weight_range[0]), float(weight_range[1])
+    if not (low.is_integer() and high.is_integer()) or high - low >= 0xFFFFFFFF:
+        raise NotImplementedError("instance_rows covers integer weight ranges narrower than 2^32 - 1")
+    seed = int(seed) & 0xFFFF_FFFF_FFFF_FFFF
+    pairs = n * (n - 1)
+    start, stop = r0 * (n - 1), r1 * (n - 1)
+    before = _count_present(seed, 0, start, float(p), threads) if start else 0
+    pres_bg = np.random.PCG64(seed)
+    pres_bg.advance(start)
+    present = np.random.Generator(pres_bg).random(stop - start) < float(p)
+    rng = int(high) - int(low)
+    wbg = np.random.PCG64(seed)
+    if rng == 0:
+        w = np.full(int(present.sum()), low)
+    else:
+        unit, half = _locate_draw(seed, pairs, before, rng, threads) if before else (pairs, 0)
+        if half == 0:
+            wbg.advance(unit)
+        else:  # the block's first draw is the buffered high half of `unit`
+            wbg.advance(unit)
+            raw = int(wbg.random_raw())
+            st = wbg.state
+            st["has_uint32"], st["uinteger"] = 1, raw >> 32
+            wbg.state = st
+        w = np.random.Generator(wbg).integers(int(low), int(high) + 1, size=int(present.sum())).astype(np.float64)
+    off = np.full(stop - start, math.inf)
+    off[present] = w
+    off = off.reshape(r1 - r0, n - 1)
+    block = np.empty((r1 - r0, n))
+    for a in range(r1 - r0):
+        i = r0 + a
+        block[a, :i] = off[a, :i]
+        block[a, i] = 0.0
+        block[a, i + 1 :] = off[a, i:]
+    return block

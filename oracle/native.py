@@ -41,6 +41,11 @@ def _load():
         lib.oracle_gemm.restype = ctypes.c_int
         lib.oracle_fw.argtypes = [ctypes.c_int, ctypes.c_int, dp, ctypes.c_int64, ctypes.c_int, ip, ip]
         lib.oracle_fw.restype = ctypes.c_int
+        fp = ctypes.POINTER(ctypes.c_float)
+        lib.oracle_closure_rows_f32.argtypes = [fp, ctypes.c_int64, fp, ctypes.c_int64, ctypes.c_int]
+        lib.oracle_closure_rows_f32.restype = ctypes.c_int
+        lib.oracle_f32_finite_range.argtypes = [fp, ctypes.c_int64, fp, fp]
+        lib.oracle_f32_finite_range.restype = None
         _lib = lib
     return _lib
 
@@ -77,3 +82,36 @@ def floyd_warshall_rounds(base, storage: str = "f64", integer: bool = False, mas
     if rc:
         raise MemoryError("oracle_fw failed")
     return d, bool(neg.value), bool(sat.value)
+
+
+def closure_rows_f32(base, rows, max_iter: int = 64):
+    """Rows ``rows`` of the min-plus closure (I (+) A)* of ``base`` (the
+    closure base, n x n oriented float32, +inf absent) by row-wise
+    Bellman-Ford in C (oracle_closure_rows_f32).  Exactness precondition,
+    checked here: every finite candidate sum stays below 2^24 in magnitude,
+    which holds when 2 * n * max|finite base| < 2^24 (a shortest path has at
+    most n-1 edges).  Returns (float64 rows, products until the fixpoint)."""
+    base = np.ascontiguousarray(base, dtype=np.float32)
+    n = base.shape[0]
+    assert base.shape == (n, n)
+    mx, mn = ctypes.c_float(0.0), ctypes.c_float(0.0)
+    _load().oracle_f32_finite_range(base.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), base.size,
+                                    ctypes.byref(mx), ctypes.byref(mn))
+    max_abs, min_fin = float(mx.value), float(mn.value)
+    if not 2.0 * n * max_abs < 2.0**24:
+        raise ValueError("closure_rows_f32 needs path sums below 2^24 (exact in float32)")
+    if min_fin < 0.0:
+        raise ValueError("closure_rows_f32 is restricted to non-negative weights (no negative cycle)")
+    r = np.ascontiguousarray(base[np.asarray(rows)], dtype=np.float32)
+    fp = ctypes.POINTER(ctypes.c_float)
+    out = []
+    its = 0
+    for s0 in range(0, r.shape[0], 16):  # 16 rows per call (register block)
+        blk = np.ascontiguousarray(r[s0 : s0 + 16])
+        it = _load().oracle_closure_rows_f32(base.ctypes.data_as(fp), n, blk.ctypes.data_as(fp), blk.shape[0],
+                                             max_iter)
+        if it < 0:
+            raise RuntimeError("closure rows did not converge")
+        out.append(blk)
+        its = max(its, it)
+    return np.concatenate(out).astype(np.float64), its

@@ -275,3 +275,42 @@ def test_small_graph_kernel_matches_general_path(cuda, dtype, monkeypatch):
         assert (got.multiplications_performed, got.negative_cycle) == (want.multiplications_performed,
                                                                        want.negative_cycle)
         assert got.distances.dist == want.distances.dist
+
+
+def test_c3_scale_fw_equals_squaring_and_oracle_rows(cuda):
+    """Config C3 at its own size (SURVEY §8(c) at-scale verification): the
+    n = 32768 instance graph_to_matrix(random_graph(n, 0.5, (1, 100),
+    instance_seed(1, n))) in int32.  The adjacency's first/last 64 rows equal
+    the reference generator (host restatement), GPU blocked FW == GPU
+    repeated squaring byte for byte, and 16 sampled distance rows equal the
+    C row-closure oracle (reference apsp.py:136-178 row by row)."""
+    from oracle.checks import closure_rows_parity
+
+    n = 32768
+    seed = instance_seed(1, n)
+    adj = random_graph_matrix(n, 0.5, (1, 100), seed, dtype=torch.int32)
+    fw = bt.floyd_warshall(adj)
+    sq = bt.apsp_by_squaring(adj)
+    assert not fw.negative_cycle and not sq.negative_cycle
+    assert fw.distances.dist == sq.distances.dist
+    rng = np.random.default_rng(0xC3)
+    rows = sorted({0, n - 1, *rng.choice(n, 14, replace=False).tolist()})
+    par = closure_rows_parity(adj.data, fw.distances.dist.data, rows, gen=(n, 0.5, (1, 100), seed))
+    assert par["generator_rows"]["mismatches"] == 0
+    assert par["closure_rows"]["mismatches"] == 0
+
+
+def test_c4_generator_rows_past_2_32(cuda):
+    """The n = 65536 instance walks n(n-1) = 4.3e9 presence doubles and
+    ~2.1e9 weight draws (past 2^31 edges and 2^32 stream positions): blocks
+    at the start, the middle and the end of the GPU-generated matrix equal
+    the host restatement of the reference stream."""
+    from oracle import graphs as og
+    from oracle.checks import mismatches, storage_to_f64
+
+    n = 65536
+    seed = instance_seed(1, n)
+    adj = random_graph_matrix(n, 0.5, (1, 100), seed, dtype=torch.float32)
+    for r0 in (0, 32768, n - 16):
+        want = og.instance_rows(n, 0.5, (1, 100), seed, r0, r0 + 16)
+        assert mismatches(storage_to_f64(adj.data[r0 : r0 + 16]).cpu().numpy(), want) == 0, r0

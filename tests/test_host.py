@@ -128,3 +128,21 @@ def test_bench_reference_arm_contract():
         assert key in line, key
     assert line["impl"] == "reference" and line["e2e"]["h2d_bytes_per_step"] == 0
     assert line["cpu_baseline"]["kind"] in ("port", "reference") and line["cpu_baseline"]["cores"] >= 1
+
+
+def test_bench_gpus_relaunch_decision():
+    """bench.py --gpus N outside torchrun re-launches itself with N ranks on
+    127.0.0.1; inside torchrun (WORLD_SIZE set) or at N = 1 it runs in place."""
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    sys.path.insert(0, str(root))
+    import bench
+
+    assert bench.relaunch_command(["--steps", "2"], 1, {}) is None
+    assert bench.relaunch_command(["--gpus", "4"], 4, {"WORLD_SIZE": "4"}) is None
+    cmd = bench.relaunch_command(["--gpus", "2", "--steps", "3"], 2, {})
+    assert cmd[:3] == [sys.executable, "-m", "torch.distributed.run"]
+    assert "--nproc-per-node=2" in cmd and "127.0.0.1" in cmd
+    assert cmd[-4:] == ["--gpus", "2", "--steps", "3"] and cmd[-5].endswith("bench.py")

@@ -303,3 +303,64 @@ def test_graph_objects_match_reference(golden):
         Graph(2, [(0, 2, 1.0)])
     with pytest.raises(ValueError):
         Graph(2, [(0, 1, math.inf)])
+
+
+def test_instance_rows_match_reference_generator(golden):
+    """oracle.graphs.instance_rows (skip-ahead row blocks: parallel presence
+    counts, Lemire draw location, numpy's own Generator for the block) equals
+    the reference instance's rows for every integer weight family of the
+    golden digests, at the first, middle and last rows."""
+    from oracle import graphs as og
+
+    for name in ("generator.npz", "generator_families.npz"):
+        g = golden(name)
+        for i in range(len(g["n"])):
+            n, p, wr, seed = int(g["n"][i]), float(g["p"][i]), (g["lo"][i], g["hi"][i]), int(g["seed"][i])
+            lo, hi = float(wr[0]), float(wr[1])
+            if not (lo.is_integer() and hi.is_integer()) or hi - lo >= 0xFFFFFFFF:
+                continue
+            full = og.random_graph_dense(n, p, wr, seed)
+            assert digest(full) == str(g["digest"][i])
+            for r0, r1 in ((0, min(n, 3)), (n // 2, min(n, n // 2 + 5)), (max(0, n - 4), n)):
+                got = og.instance_rows(n, p, wr, seed, r0, r1, threads=3)
+                assert got.tobytes() == full[r0:r1].tobytes(), (name, i, r0)
+
+
+def test_lemire32_restatement_matches_numpy():
+    from oracle import graphs as og
+
+    for rng in (1, 6, 99, 1000, 2**31 + 5, 2**32 - 3):
+        raw = np.random.PCG64(9).random_raw(1 << 14)
+        acc = og._lemire32_accept(raw, rng)
+        words = raw.view(np.uint32).astype(np.uint64)
+        vals = ((words * np.uint64(rng + 1)) >> np.uint64(32))[acc].astype(np.int64)
+        want = np.random.Generator(np.random.PCG64(9)).integers(0, rng + 1, size=len(vals))
+        assert (vals == want).all(), rng
+
+
+def test_closure_rows_c_oracle_matches_reference(golden):
+    """The C sampled-row closure (oracle_closure_rows_f32) reproduces rows of
+    the reference's apsp_by_squaring: C1 n=512 and the non-negative golden
+    graphs."""
+    from paper_1701_04733_b200.graphs import dense_rows
+
+    g = golden("c1_apsp512.npz")
+    adj = np.concatenate([b for _, b in dense_rows(512, 0.5, (1, 100), int(g["seed"][0]))])
+    rows = [0, 1, 17, 255, 300, 511]
+    got, _ = native.closure_rows_f32(ot.closure_base(adj).astype(np.float32), rows)
+    assert got.tobytes() == f64(g["sq"])[rows].tobytes()
+    s = golden("apsp_small.npz")
+    checked = 0
+    for i in range(700):
+        if f"adj{i}" not in s:
+            break
+        a = f64(s[f"adj{i}"])
+        fin = a[np.isfinite(a)]
+        if fin.size and fin.min() < 0:
+            continue
+        n = a.shape[0]
+        rows = list(range(n))[:16]
+        got, _ = native.closure_rows_f32(ot.closure_base(a).astype(np.float32), rows)
+        assert got.tobytes() == f64(s[f"sq{i}"])[rows].tobytes(), i
+        checked += 1
+    assert checked > 10
