@@ -413,13 +413,16 @@ def main(argv=None):
             result["cpu_baseline"] = {
                 "value": round(v, 4), "unit": UNIT, "cores": cores, "kind": kind,
                 "sample": f"{rows} rows x {n} x {n} ({rows * n * n:.3g} pairs, {secs:.1f} s) of the same operands; "
-                          f"btas.matmul(X[:{rows}], Y, tiles=TileSpec(32, 32, {cores})), float64 as the reference "
-                          "stores it, construction excluded",
+                          + (f"stock btas.matmul(X[:{rows}], Y, tiles=TileSpec(32, 32, {cores})) (byte-compiled "
+                             "oracle/_ref)" if kind == "reference" else
+                             f"NumPy restatement of btas.matmul, 32x32 tiles on {cores} threads")
+                          + ", float64 as the reference stores it, construction excluded",
             }
         if not args.no_parity:
             got = _checks().storage_to_f64(out[:rows]).cpu().numpy()
             result["parity"] = {"rows": rows, "cols": n, "mismatches": _checks().mismatches(got, ref),
-                                "against": f"btas.matmul ({kind}) on the same operands"}
+                                "against": ("stock btas.matmul" if kind == "reference" else "NumPy port of btas.matmul")
+                                + " on the same operands"}
         del yh
     result["_ref_gpairs"] = None  # filled below for C4's extrapolated CPU time
     if "cpu_baseline" in result:

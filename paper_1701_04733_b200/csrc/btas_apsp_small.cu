@@ -361,9 +361,16 @@ int apsp_small_typed(int integer_mode, const T* base, int64_t ldb, int64_t n, T*
   a.steps = steps;
   a.result = result;
   a.flags = flags;
-  // occupancy per instantiation (the query costs tens of microseconds; the
-  // kernel's resources, hence the answer, are the same on every B200)
-  static int per_sm = 0;
+  // co-resident CTAs per SM, per instantiation and device ordinal (the query
+  // costs tens of microseconds; a cooperative grid above the co-resident
+  // limit of the launching device fails)
+  static int per_sm_dev[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+    (void)cudaGetLastError();
+    return BTAS_ERR_CUDA;
+  }
+  int& per_sm = per_sm_dev[dev];
   if (per_sm < 1 &&
       (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apsp_small_kernel<T>, kThreads, 0) != cudaSuccess ||
        per_sm < 1)) {

@@ -39,8 +39,13 @@ template <class T> struct Traits;
 template <> struct Traits<float> {
   static constexpr int dtype = BTAS_F32;
   // integer-mode saturation limit: the reference's INT_EXACT_LIMIT (2^53,
-  // semiring.py:71) for every float storage, so an f32 result is always the
-  // reference's float64 result rounded once to f32
+  // semiring.py:71) for every float storage, so ONE f32 product / matvec /
+  // ew_add is the reference's float64 result rounded once to f32 and
+  // saturates exactly where the reference does.  Integer-valued f32 data is
+  // exact only below 2^24: in chains (matrix_power, APSP) whose sums pass
+  // 2^24 the per-step rounding compounds and the result is no longer the
+  // reference's chain rounded once (INTEGRATION.md "float32 storage";
+  // float64 or int32 storage keep integer chains exact).
   static constexpr double int_limit = 9007199254740992.0;
   BTAS_HD static float eps(bool min_plus) { return min_plus ? INFINITY : -INFINITY; }
   BTAS_HD static bool finite(float x) { return isfinite(x); }

@@ -569,15 +569,29 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
   cudaStream_t side = nullptr;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   {
+    // created together or not at all (a partial set is destroyed and the
+    // device is marked so creation is not retried on every call); they live
+    // for the thread's lifetime
     thread_local cudaStream_t t_side[64] = {};
     thread_local cudaEvent_t t_fork[64] = {}, t_join[64] = {};
+    thread_local bool t_failed[64] = {};
     int dev = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess && dev < 64) {
-      if (!t_side[dev] && (cudaStreamCreateWithFlags(&t_side[dev], cudaStreamNonBlocking) != cudaSuccess ||
-                           cudaEventCreateWithFlags(&t_fork[dev], cudaEventDisableTiming) != cudaSuccess ||
-                           cudaEventCreateWithFlags(&t_join[dev], cudaEventDisableTiming) != cudaSuccess)) {
-        (void)cudaGetLastError();
-        t_side[dev] = nullptr;
+    if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64) {
+      if (!t_side[dev] && !t_failed[dev]) {
+        cudaStream_t s = nullptr;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreateWithFlags(&e0, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&e1, cudaEventDisableTiming) == cudaSuccess) {
+          t_side[dev] = s;
+          t_fork[dev] = e0;
+          t_join[dev] = e1;
+        } else {
+          (void)cudaGetLastError();
+          if (e0) cudaEventDestroy(e0);
+          if (s) cudaStreamDestroy(s);
+          t_failed[dev] = true;
+        }
       }
       side = t_side[dev];
       fork_ev = t_fork[dev];
@@ -586,6 +600,24 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
       (void)cudaGetLastError();
     }
   }
+  // Joins the side stream back into the caller's stream on every exit from
+  // a forked region, including early error returns, so the caller's stream
+  // is always ordered after the side stream's work.
+  struct Join {
+    cudaStream_t st = nullptr, side = nullptr;
+    cudaEvent_t ev = nullptr;
+    bool open = false;
+    int close() {
+      if (!open) return BTAS_OK;
+      open = false;
+      if (cudaEventRecord(ev, side) != cudaSuccess || cudaStreamWaitEvent(st, ev, 0) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return BTAS_ERR_CUDA;
+      }
+      return BTAS_OK;
+    }
+    ~Join() { (void)close(); }
+  };
   auto phases12 = [&](int kb, int slot) -> int {
     f.k0 = (int64_t)kb * b;
     f.koff = slot * b;
@@ -614,9 +646,17 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
       const int64_t kk = (int64_t)kb * b, mk = std::min<int64_t>(b, n - kk);
       if (j > 0) {
         const bool fork = side != nullptr;
-        if (fork &&
-            (cudaEventRecord(fork_ev, st) != cudaSuccess || cudaStreamWaitEvent(side, fork_ev, 0) != cudaSuccess))
-          return BTAS_ERR_CUDA;
+        Join join;
+        if (fork) {
+          if (cudaEventRecord(fork_ev, st) != cudaSuccess || cudaStreamWaitEvent(side, fork_ev, 0) != cudaSuccess) {
+            (void)cudaGetLastError();
+            return BTAS_ERR_CUDA;
+          }
+          join.st = st;
+          join.side = side;
+          join.ev = join_ev;
+          join.open = true;
+        }
         {  // pending updates -> row block kb
           GemmArgs a = g, a16 = g16;
           a.M = a16.M = mk;
@@ -639,9 +679,7 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
           a.skip_row_hi = a16.skip_row_hi = kk + b;
           if ((rc = phase3_on(a, a16, j, fork ? side : st))) return rc;
         }
-        if (fork &&
-            (cudaEventRecord(join_ev, side) != cudaSuccess || cudaStreamWaitEvent(st, join_ev, 0) != cudaSuccess))
-          return BTAS_ERR_CUDA;
+        if ((rc = join.close())) return rc;
       }
       if ((rc = phases12(kb, j))) return rc;
     }

@@ -21,17 +21,25 @@
 
 namespace btas {
 
+// SM count of the CURRENT device, cached per device ordinal (one process may
+// drive several GPUs; a MIG slice or a mixed box has different counts).
 int device_sm_count() {
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) {
-      (void)cudaGetLastError();
-      sms = 148;
-    }
+  constexpr int kMaxDev = 64;
+  static int sms[kMaxDev] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    (void)cudaGetLastError();
+    dev = 0;
   }
-  return sms;
+  int* slot = dev >= 0 && dev < kMaxDev ? &sms[dev] : nullptr;
+  if (slot && *slot > 0) return *slot;
+  int v = 0;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) {
+    (void)cudaGetLastError();
+    v = 148;
+  }
+  if (slot) *slot = v;
+  return v;
 }
 
 // Optional CUDA-event bracketing of the GEMM kernel launches (bench.py's

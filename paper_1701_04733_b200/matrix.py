@@ -189,45 +189,69 @@ class _FlagLedger:
     """Set-only device flag words (dev_flags of the C ABI), read lazily.
 
     Every kernel call gets a fresh int32[NUM_FLAGS] buffer; the ones whose
-    saturation bit has not been read yet are kept here so that
+    saturation bit has not been read yet are kept here, each with the CUDA
+    stream that was current when the kernel writing it was launched, so that
     ``saturation_seen()`` can fold them in with a single synchronising read.
+    Reads and folds run on the reader's current stream after making it wait
+    for every producing stream (a flag written by a kernel on another stream
+    or thread is never read before that kernel ran), and the folded buffers
+    are marked used on the reader's stream for the caching allocator.
     """
 
     def __init__(self):
-        self._pending: "list[torch.Tensor]" = []
+        self._pending: "list[tuple[torch.Tensor, torch.cuda.Stream]]" = []
         self._lock = threading.Lock()
 
     def new(self, device: torch.device) -> torch.Tensor:
         return torch.zeros(_lib.NUM_FLAGS, dtype=torch.int32, device=device)
 
     def track(self, flags: torch.Tensor) -> None:
+        """Call right after launching the kernel(s) that write ``flags``, on
+        the stream they were launched on (the current one)."""
+        entry = (flags, torch.cuda.current_stream(flags.device))
         with self._lock:
-            self._pending.append(flags)
+            self._pending.append(entry)
             if len(self._pending) > 256:
                 self._fold_locked()
 
+    @staticmethod
+    def _by_device(pending):
+        by_dev: "dict[torch.device, list]" = {}
+        for f, s in pending:
+            by_dev.setdefault(f.device, []).append((f, s))
+        return by_dev
+
+    @staticmethod
+    def _gather_sat(dev, entries) -> torch.Tensor:
+        """max of the saturation words of ``entries`` on ``dev``'s current
+        stream, ordered after every producing stream."""
+        cur = torch.cuda.current_stream(dev)
+        waited = set()
+        for f, s in entries:
+            if s.cuda_stream != cur.cuda_stream:
+                if s.cuda_stream not in waited:
+                    cur.wait_stream(s)
+                    waited.add(s.cuda_stream)
+                f.record_stream(cur)
+        return torch.stack([f[_lib.FLAG_SATURATED] for f, _ in entries]).amax()
+
     def _fold_locked(self) -> None:
-        by_dev: "dict[torch.device, list[torch.Tensor]]" = {}
-        for f in self._pending:
-            by_dev.setdefault(f.device, []).append(f)
         folded = []
-        for dev, fs in by_dev.items():
-            sat = torch.stack([f[_lib.FLAG_SATURATED] for f in fs]).amax()
-            out = torch.zeros(_lib.NUM_FLAGS, dtype=torch.int32, device=dev)
-            out[_lib.FLAG_SATURATED] = sat
-            folded.append(out)
+        for dev, entries in self._by_device(self._pending).items():
+            with torch.cuda.device(dev):
+                sat = self._gather_sat(dev, entries)
+                out = torch.zeros(_lib.NUM_FLAGS, dtype=torch.int32, device=dev)
+                out[_lib.FLAG_SATURATED] = sat
+                folded.append((out, torch.cuda.current_stream(dev)))
         self._pending = folded
 
     def read_saturation(self) -> bool:
         with self._lock:
             pending, self._pending = self._pending, []
-        by_dev: "dict[torch.device, list[torch.Tensor]]" = {}
-        for f in pending:
-            by_dev.setdefault(f.device, []).append(f)
         seen = False
-        for dev, fs in by_dev.items():
+        for dev, entries in self._by_device(pending).items():
             with torch.cuda.device(dev):
-                sat = torch.stack([f[_lib.FLAG_SATURATED] for f in fs]).amax().reshape(1)
+                sat = self._gather_sat(dev, entries).reshape(1)
                 seen |= int(_host_read(sat)[0]) != 0
         return seen
 

@@ -128,6 +128,31 @@ def test_saturation_kats_f64(cuda, golden):
     assert not bt.saturation_seen()
 
 
+def test_saturation_seen_across_streams(cuda):
+    """A saturating product launched on a side stream (behind a long GEMM on
+    that stream) is seen by saturation_seen() called from the default stream
+    — also after the ledger folded more than 256 pending flag buffers."""
+    big = float(2**53 - 1)
+    n = 4096
+    rng = np.random.default_rng(12)
+    x = bt.TropicalMatrix(MIN, rand_sym(rng, n, n), dtype=torch.float32)
+    a = bt.TropicalMatrix(MIN, [[big]])
+    side = torch.cuda.Stream()
+    for folds in (False, True):
+        bt.reset_saturation()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(side):
+            for _ in range(3):
+                bt.matmul(x, x)  # keeps the side stream busy
+            bt.matmul(a, a)  # saturates
+            if folds:
+                small = bt.TropicalMatrix(MIN, [[1.0]])
+                for _ in range(300):
+                    bt.matmul(small, small)
+        assert bt.saturation_seen(), folds
+    torch.cuda.synchronize()
+
+
 @pytest.mark.parametrize("dtype,big", [(torch.float32, 3e38), (torch.int32, 2**28 - 1), (torch.float64, 1e308)])
 @pytest.mark.parametrize("kind", [MIN, MAX])
 def test_saturation_per_storage(cuda, dtype, big, kind):
