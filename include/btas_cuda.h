@@ -177,6 +177,20 @@ int btas_matvec(int dtype, int kind, int integer_mode,
                 const void* V, int64_t ldv, int64_t batch,
                 void* Out, int64_t ldo, int32_t* dev_flags, btas_stream_t stream);
 
+/* btas_matvec with a caller-known bound: abs_bound >= max|finite A| +
+ * max|finite V| (e.g. from the btas_stats.max_abs_key of each operand's
+ * ingest, which immutable operands keep).  When the bound proves that no
+ * finite (x) finite candidate can overflow (below 2^28 for int32, the
+ * integer limit in integer mode, the largest finite value otherwise) the
+ * kernels skip the per-element magnitude screen of matrix.py:408-420's mask
+ * (the result and the flag are the same: nothing can saturate).  A negative
+ * or NaN abs_bound means "unknown" = btas_matvec. */
+int btas_matvec_bounded(int dtype, int kind, int integer_mode,
+                        const void* A, int64_t lda, int64_t M, int64_t K,
+                        const void* V, int64_t ldv, int64_t batch,
+                        void* Out, int64_t ldo, double abs_bound,
+                        int32_t* dev_flags, btas_stream_t stream);
+
 /* Blocked three-phase Floyd-Warshall, in place on D (n x n, min-plus),
  * bit-identical to the sequential k-round program of apsp.py:93-133
  * (snapshot panels keep each round's operands exactly as the reference sees

@@ -112,6 +112,7 @@ SIGNATURES = {
     "btas_gemm_timing": (_i32, [_i32]),
     "btas_gemm_timing_read": (_i32, [ctypes.POINTER(_dbl), ctypes.POINTER(_i32)]),
     "btas_matvec": (_i32, [_i32, _i32, _i32, _p, _i64, _i64, _i64, _p, _i64, _i64, _p, _i64, _p, _p]),
+    "btas_matvec_bounded": (_i32, [_i32, _i32, _i32, _p, _i64, _i64, _i64, _p, _i64, _i64, _p, _i64, _dbl, _p, _p]),
     "btas_fw_workspace_bytes": (_sz, [_i32, _i64]),
     "btas_fw": (_i32, [_i32, _i32, _p, _i64, _i64, _i32, _dbl, _dbl, _p, _p, _sz, _p]),
     "btas_fw_dist_workspace_bytes": (_sz, [_i32, _i64, _i64, ctypes.POINTER(_sz), ctypes.POINTER(_sz)]),

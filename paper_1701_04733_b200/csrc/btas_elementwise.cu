@@ -3,6 +3,7 @@
 // All are grid-stride, 16-byte vectorised where alignment allows, and sized
 // to a multiple of the SM count.
 #include <algorithm>
+#include <cfloat>
 #include <cuda.h>
 #include <type_traits>
 
@@ -179,7 +180,8 @@ BTAS_D void mv_acc(T& acc, T a, T v, int int_mode, double limit, bool& sat) {
 }
 
 // one pass over the CTA's R rows; returns the thread's max|finite| of A and V
-template <class T, bool MIN, int R, int NB, bool CHECKED>
+// (tracked only when SCREEN: a caller-proven bound makes the screen moot)
+template <class T, bool MIN, int R, int NB, bool CHECKED, bool SCREEN = true>
 BTAS_D void mv_pass(const T* __restrict__ A, int64_t lda, int64_t M, int64_t K, const T* __restrict__ Vv,
                     int64_t ldv, int nb, int64_t r0, int64_t kvec_end, int int_mode, double limit,
                     T (&acc)[R][NB], T& amax, T& vmax, bool& sat) {
@@ -194,7 +196,7 @@ BTAS_D void mv_pass(const T* __restrict__ A, int64_t lda, int64_t M, int64_t K, 
 #pragma unroll
         for (int e = 0; e < VEC; ++e) {
           vv[b][e] = p[e];
-          if (!CHECKED) vmax = max(vmax, abs_finite(p[e]));
+          if (!CHECKED && SCREEN) vmax = max(vmax, abs_finite(p[e]));
         }
       }
     }
@@ -209,7 +211,7 @@ BTAS_D void mv_pass(const T* __restrict__ A, int64_t lda, int64_t M, int64_t K, 
       const T* ap = reinterpret_cast<const T*>(&au[r]);
 #pragma unroll
       for (int e = 0; e < VEC; ++e)
-        if (!CHECKED) amax = max(amax, abs_finite(ap[e]));
+        if (!CHECKED && SCREEN) amax = max(amax, abs_finite(ap[e]));
       if constexpr (!CHECKED && Traits<T>::dtype == BTAS_F32) {
         // f32: FADD2 over a pair of k, then one FMNMX3 into the accumulator
 #pragma unroll
@@ -232,12 +234,12 @@ BTAS_D void mv_pass(const T* __restrict__ A, int64_t lda, int64_t M, int64_t K, 
   for (int64_t k = kvec_end + threadIdx.x; k < K; k += blockDim.x) {
 #pragma unroll
     for (int b = 0; b < NB; ++b)
-      if (b < nb && !CHECKED) vmax = max(vmax, abs_finite(Vv[(int64_t)b * ldv + k]));
+      if (b < nb && !CHECKED && SCREEN) vmax = max(vmax, abs_finite(Vv[(int64_t)b * ldv + k]));
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int64_t row = r0 + r < M ? r0 + r : M - 1;
       const T a = A[row * lda + k];
-      if (!CHECKED) amax = max(amax, abs_finite(a));
+      if (!CHECKED && SCREEN) amax = max(amax, abs_finite(a));
 #pragma unroll
       for (int b = 0; b < NB; ++b)
         if (b < nb) mv_acc<T, MIN, CHECKED>(acc[r][b], a, Vv[(int64_t)b * ldv + k], int_mode, limit, sat);
@@ -260,7 +262,10 @@ BTAS_D T block_max(T v, T* scratch) {
   return m;
 }
 
-template <class T, bool MIN, int R, int NB>
+// SCREEN = false: the caller proved max|finite A| + max|finite V| below the
+// overflow limit (btas_matvec_bounded), so no candidate can overflow and the
+// magnitude tracking and the masked rerun are compiled out.
+template <class T, bool MIN, int R, int NB, bool SCREEN = true>
 __global__ void __launch_bounds__(256) matvec_kernel(const T* __restrict__ A, int64_t lda, int64_t M, int64_t K,
                                                      const T* __restrict__ Vv, int64_t ldv, int nb,
                                                      T* __restrict__ Out, int64_t ldo, int int_mode, double limit,
@@ -278,17 +283,20 @@ __global__ void __launch_bounds__(256) matvec_kernel(const T* __restrict__ A, in
                       ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(Vv)) & 15) == 0;
   const int64_t kvec_end = vec_ok ? (K / VEC) * VEC : 0;
   T amax = 0, vmax = 0;
-  mv_pass<T, MIN, R, NB, false>(A, lda, M, K, Vv, ldv, nb, r0, kvec_end, int_mode, limit, acc, amax, vmax, sat);
-  // exact screen: |a + v| <= amax + vmax for every finite pair of this CTA
-  __shared__ T scratch[8];
-  amax = block_max(amax, scratch);
-  vmax = block_max(vmax, scratch);
-  bool possible;
-  if constexpr (Traits<T>::dtype == BTAS_I32) {
-    possible = (int64_t)amax + (int64_t)vmax >= (int64_t)kI32Limit;
-  } else {
-    const T bound = amax + vmax;  // storage arithmetic, rounding is monotone
-    possible = int_mode ? ((double)bound >= limit) : isinf(bound);
+  mv_pass<T, MIN, R, NB, false, SCREEN>(A, lda, M, K, Vv, ldv, nb, r0, kvec_end, int_mode, limit, acc, amax, vmax,
+                                        sat);
+  bool possible = false;
+  if constexpr (SCREEN) {
+    // exact screen: |a + v| <= amax + vmax for every finite pair of this CTA
+    __shared__ T scratch[8];
+    amax = block_max(amax, scratch);
+    vmax = block_max(vmax, scratch);
+    if constexpr (Traits<T>::dtype == BTAS_I32) {
+      possible = (int64_t)amax + (int64_t)vmax >= (int64_t)kI32Limit;
+    } else {
+      const T bound = amax + vmax;  // storage arithmetic, rounding is monotone
+      possible = int_mode ? ((double)bound >= limit) : isinf(bound);
+    }
   }
   if (possible) {  // uniform across the CTA
 #pragma unroll
@@ -370,7 +378,7 @@ BTAS_D T key_abs(int32_t k) {
   else return (T)(k >> 2);
 }
 
-template <class T, bool MIN>
+template <class T, bool MIN, bool SCREEN = true>
 __global__ void __launch_bounds__(kWideThreads, 2) matvec_wide_kernel(const __grid_constant__ CUtensorMap mapA,
                                                                    const __grid_constant__ CUtensorMap mapV,
                                                                    const T* __restrict__ A, int64_t lda, int64_t M,
@@ -427,7 +435,7 @@ __global__ void __launch_bounds__(kWideThreads, 2) matvec_wide_kernel(const __gr
         v[b][1] = __builtin_bit_cast(T, u.y);
         v[b][2] = __builtin_bit_cast(T, u.z);
         v[b][3] = __builtin_bit_cast(T, u.w);
-        if (warp == 0 && b < nb) {
+        if (SCREEN && warp == 0 && b < nb) {
 #pragma unroll
           for (int e = 0; e < 4; ++e) vkey = max(vkey, abs_key(v[b][e]));
         }
@@ -443,7 +451,8 @@ __global__ void __launch_bounds__(kWideThreads, 2) matvec_wide_kernel(const __gr
       for (int r = 0; r < 4; ++r) {
         const T a[4] = {__builtin_bit_cast(T, au[r].x), __builtin_bit_cast(T, au[r].y), __builtin_bit_cast(T, au[r].z),
                         __builtin_bit_cast(T, au[r].w)};
-        akey = max(akey, max(max(abs_key(a[0]), abs_key(a[1])), max(abs_key(a[2]), abs_key(a[3]))));
+        if constexpr (SCREEN)
+          akey = max(akey, max(max(abs_key(a[0]), abs_key(a[1])), max(abs_key(a[2]), abs_key(a[3]))));
 #pragma unroll
         for (int b = 0; b < kWideNB; ++b) {
           if constexpr (Traits<T>::dtype == BTAS_F32) {
@@ -465,17 +474,19 @@ __global__ void __launch_bounds__(kWideThreads, 2) matvec_wide_kernel(const __gr
       issue(c + kWideStages);
     }
   }
-  T amax = key_abs<T>(akey), vmax = key_abs<T>(vkey);
-  // exact screen over the CTA (see matvec_kernel)
-  __shared__ T scratch[kWideThreads / 32];
-  amax = block_max(amax, scratch);
-  vmax = block_max(vmax, scratch);
-  bool possible;
-  if constexpr (Traits<T>::dtype == BTAS_I32) {
-    possible = (int64_t)amax + (int64_t)vmax >= (int64_t)kI32Limit;
-  } else {
-    const T bound = amax + vmax;
-    possible = int_mode ? ((double)bound >= limit) : isinf(bound);
+  bool possible = false;
+  if constexpr (SCREEN) {
+    T amax = key_abs<T>(akey), vmax = key_abs<T>(vkey);
+    // exact screen over the CTA (see matvec_kernel)
+    __shared__ T scratch[kWideThreads / 32];
+    amax = block_max(amax, scratch);
+    vmax = block_max(vmax, scratch);
+    if constexpr (Traits<T>::dtype == BTAS_I32) {
+      possible = (int64_t)amax + (int64_t)vmax >= (int64_t)kI32Limit;
+    } else {
+      const T bound = amax + vmax;
+      possible = int_mode ? ((double)bound >= limit) : isinf(bound);
+    }
   }
   if (!possible) {
 #pragma unroll
@@ -574,9 +585,21 @@ inline bool wide_tensor_map(CUtensorMap* m, bool f32, const void* base, int64_t 
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <class T, bool MIN>
-int matvec_typed(int int_mode, const T* A, int64_t lda, int64_t M, int64_t K, const T* V, int64_t ldv,
-                 int64_t batch, T* Out, int64_t ldo, int32_t* flags, cudaStream_t st) {
+// true when a caller bound B >= max|finite A| + max|finite V| proves that no
+// finite (x) finite candidate overflows: |a + v| <= B below the integer limit
+// (integer mode, int32) or below the largest finite value of the storage
+// (a sum of magnitude below it rounds to a finite value)
+template <class T>
+bool bound_proves_no_overflow(double abs_bound, int int_mode) {
+  if (!(abs_bound >= 0.0)) return false;  // unknown (negative or NaN)
+  if constexpr (Traits<T>::dtype == BTAS_I32) return abs_bound < (double)kI32Limit;
+  if (int_mode) return abs_bound < Traits<T>::int_limit;
+  return abs_bound < (double)(Traits<T>::dtype == BTAS_F32 ? FLT_MAX : DBL_MAX);
+}
+
+template <class T, bool MIN, bool SCREEN>
+int matvec_launch(int int_mode, const T* A, int64_t lda, int64_t M, int64_t K, const T* V, int64_t ldv,
+                  int64_t batch, T* Out, int64_t ldo, int32_t* flags, cudaStream_t st) {
   const double limit = Traits<T>::dtype == BTAS_I32 ? (double)kI32Limit : Traits<T>::int_limit;
   // 5-8 vectors of 4-byte storage: one pass (matvec_wide_kernel) when the
   // shapes allow 16-byte chunked streaming; otherwise up to 4 vectors per
@@ -597,32 +620,40 @@ int matvec_typed(int int_mode, const T* A, int64_t lda, int64_t M, int64_t K, co
           return BTAS_ERR_CUDA;
         static unsigned long long configured = 0;
         if (!configured_on_current_device(configured)) {
-          if (cudaFuncSetAttribute(matvec_wide_kernel<T, MIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+          if (cudaFuncSetAttribute(matvec_wide_kernel<T, MIN, SCREEN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)kWideSmem) != cudaSuccess) {
             (void)cudaGetLastError();
             return BTAS_ERR_CUDA;
           }
           mark_configured(configured);
         }
-        matvec_wide_kernel<T, MIN><<<(unsigned)ceil_div(M, kWideRows), kWideThreads, kWideSmem, st>>>(
+        matvec_wide_kernel<T, MIN, SCREEN><<<(unsigned)ceil_div(M, kWideRows), kWideThreads, kWideSmem, st>>>(
             mapA, mapV, A, lda, M, K, Vb, ldv, nb, Ob, ldo, int_mode, limit, flags);
         BTAS_CUDA_CHECK_LAUNCH();
         continue;
       }
     }
     if (nb == 1) {
-      matvec_kernel<T, MIN, 16, 1><<<(unsigned)ceil_div(M, 16), 256, 0, st>>>(A, lda, M, K, Vb, ldv, nb, Ob, ldo,
+      matvec_kernel<T, MIN, 16, 1, SCREEN><<<(unsigned)ceil_div(M, 16), 256, 0, st>>>(A, lda, M, K, Vb, ldv, nb, Ob, ldo,
                                                                             int_mode, limit, flags);
     } else if (nb <= 2) {
-      matvec_kernel<T, MIN, 8, 2><<<(unsigned)ceil_div(M, 8), 256, 0, st>>>(A, lda, M, K, Vb, ldv, nb, Ob, ldo,
+      matvec_kernel<T, MIN, 8, 2, SCREEN><<<(unsigned)ceil_div(M, 8), 256, 0, st>>>(A, lda, M, K, Vb, ldv, nb, Ob, ldo,
                                                                           int_mode, limit, flags);
     } else if (nb <= 4) {
-      matvec_kernel<T, MIN, 8, 4><<<(unsigned)ceil_div(M, 8), 256, 0, st>>>(A, lda, M, K, Vb, ldv, nb, Ob, ldo,
+      matvec_kernel<T, MIN, 8, 4, SCREEN><<<(unsigned)ceil_div(M, 8), 256, 0, st>>>(A, lda, M, K, Vb, ldv, nb, Ob, ldo,
                                                                           int_mode, limit, flags);
     }
     BTAS_CUDA_CHECK_LAUNCH();
   }
   return BTAS_OK;
+}
+
+template <class T, bool MIN>
+int matvec_typed(int int_mode, double abs_bound, const T* A, int64_t lda, int64_t M, int64_t K, const T* V,
+                 int64_t ldv, int64_t batch, T* Out, int64_t ldo, int32_t* flags, cudaStream_t st) {
+  return bound_proves_no_overflow<T>(abs_bound, int_mode)
+             ? matvec_launch<T, MIN, false>(int_mode, A, lda, M, K, V, ldv, batch, Out, ldo, flags, st)
+             : matvec_launch<T, MIN, true>(int_mode, A, lda, M, K, V, ldv, batch, Out, ldo, flags, st);
 }
 
 inline bool valid_dtype(int d) { return d == BTAS_F32 || d == BTAS_I32 || d == BTAS_F64; }
@@ -798,9 +829,9 @@ extern "C" int btas_diag_negative(int dtype, const void* d, int64_t ld, int64_t 
   return BTAS_OK;
 }
 
-extern "C" int btas_matvec(int dtype, int kind, int integer_mode, const void* A, int64_t lda, int64_t M, int64_t K,
-                           const void* V, int64_t ldv, int64_t batch, void* Out, int64_t ldo, int32_t* flags,
-                           btas_stream_t stream) {
+extern "C" int btas_matvec_bounded(int dtype, int kind, int integer_mode, const void* A, int64_t lda, int64_t M,
+                                   int64_t K, const void* V, int64_t ldv, int64_t batch, void* Out, int64_t ldo,
+                                   double abs_bound, int32_t* flags, btas_stream_t stream) {
   if (!A || !V || !Out || !flags || M < 1 || K < 1 || batch < 1 || lda < K || ldv < K || ldo < M ||
       !valid_kind(kind))
     return BTAS_ERR_INVALID;
@@ -808,10 +839,16 @@ extern "C" int btas_matvec(int dtype, int kind, int integer_mode, const void* A,
   const bool mn = kind == BTAS_MIN_PLUS;
   int rc = BTAS_OK;
   BTAS_DISPATCH(dtype, {
-    rc = mn ? matvec_typed<T, true>(integer_mode, (const T*)A, lda, M, K, (const T*)V, ldv, batch, (T*)Out, ldo,
-                                    flags, st)
-            : matvec_typed<T, false>(integer_mode, (const T*)A, lda, M, K, (const T*)V, ldv, batch, (T*)Out, ldo,
-                                     flags, st);
+    rc = mn ? matvec_typed<T, true>(integer_mode, abs_bound, (const T*)A, lda, M, K, (const T*)V, ldv, batch,
+                                    (T*)Out, ldo, flags, st)
+            : matvec_typed<T, false>(integer_mode, abs_bound, (const T*)A, lda, M, K, (const T*)V, ldv, batch,
+                                     (T*)Out, ldo, flags, st);
   })
   return rc;
+}
+
+extern "C" int btas_matvec(int dtype, int kind, int integer_mode, const void* A, int64_t lda, int64_t M, int64_t K,
+                           const void* V, int64_t ldv, int64_t batch, void* Out, int64_t ldo, int32_t* flags,
+                           btas_stream_t stream) {
+  return btas_matvec_bounded(dtype, kind, integer_mode, A, lda, M, K, V, ldv, batch, Out, ldo, -1.0, flags, stream);
 }

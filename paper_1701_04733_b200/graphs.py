@@ -37,6 +37,7 @@ from .matrix import (
     _ptr,
     _read_stats,
     _resolve_device,
+    _stats_bound,
     _stream,
     get_default_dtype,
 )
@@ -175,7 +176,10 @@ def _random_graph_matrix(n: int, p: float, weight_range, seed: int, *, dtype: "t
     if st.out_of_range:
         raise ValueError(f"instance weights do not fit {dt} storage")
     integer = dt == torch.int32 or (st.non_integral == 0 and st.over_limit == 0)
-    return TropicalMatrix._wrap(SemiringKind.MIN_PLUS, out, integer)
+    # the validation-free fill of exactly representable integer weights
+    # leaves the statistics empty; its entries are 0, Infinity or in [low, high]
+    bound = _stats_bound(st) if st.finite_count else max(abs(low), abs(high))
+    return TropicalMatrix._wrap(SemiringKind.MIN_PLUS, out, integer, bound)
 
 
 def random_graph_matrix_host(n: int, p: float, weight_range, seed: int, *, dtype: "torch.dtype | None" = None,
@@ -196,7 +200,7 @@ def random_graph_matrix_host(n: int, p: float, weight_range, seed: int, *, dtype
     if st.out_of_range:
         raise ValueError(f"instance weights do not fit {dt} storage")
     integer = dt == torch.int32 or (st.non_integral == 0 and st.over_limit == 0)
-    return TropicalMatrix._wrap(kind, out, integer)
+    return TropicalMatrix._wrap(kind, out, integer, _stats_bound(st))
 
 
 def edges_to_matrix(n: int, src, dst, weight, *, dtype: "torch.dtype | None" = None, device=None) -> TropicalMatrix:
@@ -249,7 +253,7 @@ def _edges_to_matrix(n: int, src, dst, weight, *, dtype: "torch.dtype | None" = 
         raise ValueError(f"entries do not fit {dt} storage")
     st = _read_stats(stats)
     integer = dt == torch.int32 or (st.non_integral == 0 and st.over_limit == 0)
-    return TropicalMatrix._wrap(SemiringKind.MIN_PLUS, out, integer)
+    return TropicalMatrix._wrap(SemiringKind.MIN_PLUS, out, integer, _stats_bound(st))
 
 
 def graph_to_matrix(g, *, dtype: "torch.dtype | None" = None, device=None) -> TropicalMatrix:

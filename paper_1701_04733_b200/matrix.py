@@ -384,6 +384,25 @@ def _integer_flag(st: _lib.Stats, requested, dtype: torch.dtype) -> bool:
     return True
 
 
+def _stats_bound(st: _lib.Stats) -> float:
+    """max |finite stored value| from ingest statistics (0 when none)."""
+    return _lib.key_to_float(st.max_abs_key) if st.finite_count else 0.0
+
+
+def _sum_bound(*bounds: "float | None") -> "float | None":
+    """|a ⊗ b| <= |a| + |b| for finite entries: the bound of a product's
+    finite results (None when an operand's bound is unknown)."""
+    if any(b is None for b in bounds):
+        return None
+    return float(sum(bounds))
+
+
+def _max_bound(*bounds: "float | None") -> "float | None":
+    if any(b is None for b in bounds):
+        return None
+    return float(max(bounds))
+
+
 def _symbolic(v: float) -> float:
     return math.inf if math.isinf(v) else v
 
@@ -399,9 +418,14 @@ class TropicalMatrix:
     objects.  integer=None auto-detects exact-integer mode, True demands it,
     False disables it (reference matrix.py:122-156).  ``dtype`` selects the
     storage (float64 default, float32, int32), ``device`` the GPU.
+
+    ``abs_bound`` is an upper bound on max |finite entry| (exact for ingested
+    matrices, propagated through products and ⊕; None when unknown): the
+    matvec kernels use it to skip their overflow screen (immutable data, so
+    the bound never goes stale).
     """
 
-    __slots__ = ("kind", "data", "integer")
+    __slots__ = ("kind", "data", "integer", "abs_bound")
 
     def __init__(self, kind: SemiringKind, rows: object, integer: "bool | None" = None, *,
                  dtype: "torch.dtype | None" = None, device=None):
@@ -411,21 +435,23 @@ class TropicalMatrix:
         _dtype_code(dt)
         dev = _resolve_device(device)
         data, st = _ingest(kind, rows, dt, dev, 2)
-        self._fix(kind, data, _integer_flag(st, integer, dt))
+        self._fix(kind, data, _integer_flag(st, integer, dt), _stats_bound(st))
 
-    def _fix(self, kind: SemiringKind, data: torch.Tensor, integer: bool) -> None:
+    def _fix(self, kind: SemiringKind, data: torch.Tensor, integer: bool, abs_bound: "float | None" = None) -> None:
         object.__setattr__(self, "kind", kind)
         object.__setattr__(self, "data", data)
         object.__setattr__(self, "integer", bool(integer))
+        object.__setattr__(self, "abs_bound", abs_bound)
 
     def __setattr__(self, name: str, value: object) -> None:
         raise AttributeError("TropicalMatrix is immutable")
 
     @classmethod
-    def _wrap(cls, kind: SemiringKind, data: torch.Tensor, integer: bool) -> "TropicalMatrix":
+    def _wrap(cls, kind: SemiringKind, data: torch.Tensor, integer: bool,
+              abs_bound: "float | None" = None) -> "TropicalMatrix":
         """Adopt already-oriented device storage (internal)."""
         self = object.__new__(cls)
-        self._fix(kind, data, integer)
+        self._fix(kind, data, integer, abs_bound)
         return self
 
     @classmethod
@@ -447,7 +473,7 @@ class TropicalMatrix:
         _lib.call("btas_fill", _dtype_code(dt), _kind_code(kind), _ptr(data), data.numel(), value, _stream(dev))
         stored = float(np.float32(value)) if dt == torch.float32 else value
         integer = dt == torch.int32 or math.isinf(value) or (stored == math.floor(stored) and abs(stored) < 2**53)
-        return cls._wrap(kind, data, integer)
+        return cls._wrap(kind, data, integer, 0.0 if math.isinf(stored) else abs(stored))
 
     # -- shape / access ------------------------------------------------------
     @property
@@ -509,7 +535,7 @@ class TropicalMatrix:
 class TropicalVector:
     """Immutable dense vector on a GPU; same conventions as TropicalMatrix."""
 
-    __slots__ = ("kind", "data", "integer")
+    __slots__ = ("kind", "data", "integer", "abs_bound")
 
     def __init__(self, kind: SemiringKind, values: object, integer: "bool | None" = None, *,
                  dtype: "torch.dtype | None" = None, device=None):
@@ -519,17 +545,19 @@ class TropicalVector:
         _dtype_code(dt)
         dev = _resolve_device(device)
         data, st = _ingest(kind, values, dt, dev, 1)
-        self._fix(kind, data, _integer_flag(st, integer, dt))
+        self._fix(kind, data, _integer_flag(st, integer, dt), _stats_bound(st))
 
-    def _fix(self, kind, data, integer) -> None:
+    def _fix(self, kind, data, integer, abs_bound=None) -> None:
         object.__setattr__(self, "kind", kind)
         object.__setattr__(self, "data", data)
         object.__setattr__(self, "integer", bool(integer))
+        object.__setattr__(self, "abs_bound", abs_bound)
 
     @classmethod
-    def _wrap(cls, kind: SemiringKind, data: torch.Tensor, integer: bool) -> "TropicalVector":
+    def _wrap(cls, kind: SemiringKind, data: torch.Tensor, integer: bool,
+              abs_bound: "float | None" = None) -> "TropicalVector":
         self = object.__new__(cls)
-        self._fix(kind, data, integer)
+        self._fix(kind, data, integer, abs_bound)
         return self
 
     def __setattr__(self, name: str, value: object) -> None:
@@ -602,7 +630,7 @@ def identity_matrix(kind: SemiringKind, n: int, *, dtype: "torch.dtype | None" =
     data = torch.empty((n, n), dtype=dt, device=dev)
     with _device_ctx(dev):
         _lib.call("btas_identity", _dtype_code(dt), _kind_code(kind), _ptr(data), n, n, _stream(dev))
-    return TropicalMatrix._wrap(kind, data, True)
+    return TropicalMatrix._wrap(kind, data, True, 0.0)
 
 
 def _check_same_kind(a, b) -> None:
@@ -636,7 +664,7 @@ def ew_add(a, b):
     out = torch.empty_like(x)
     _lib.call("btas_ewadd", _dtype_code(x.dtype), _kind_code(a.kind), _ptr(x), _ptr(y), _ptr(out), x.numel(),
               _stream(x.device))
-    return type(a)._wrap(a.kind, out, a.integer and b.integer)
+    return type(a)._wrap(a.kind, out, a.integer and b.integer, _max_bound(a.abs_bound, b.abs_bound))
 
 
 def _gemm(x: torch.Tensor, y: torch.Tensor, kind: SemiringKind, integer: bool, *, z: "torch.Tensor | None" = None,
@@ -710,7 +738,10 @@ def matmul(x: TropicalMatrix, y: TropicalMatrix, accumulate_into: "TropicalMatri
         raise TypeError(f"tiles must be a TileSpec, got {type(tiles).__name__}")
     _check_same_storage(x, y)
     out, _ = _gemm(_rowmajor(x.data), _rowmajor(y.data), x.kind, integer, z=z)
-    return TropicalMatrix._wrap(x.kind, out, integer)
+    bound = _sum_bound(x.abs_bound, y.abs_bound)
+    if accumulate_into is not None:
+        bound = _max_bound(bound, accumulate_into.abs_bound)
+    return TropicalMatrix._wrap(x.kind, out, integer, bound)
 
 
 @_on_operand_device
@@ -720,18 +751,22 @@ def matvec(a: TropicalMatrix, v: TropicalVector) -> TropicalVector:
     if a.n_cols != len(v):
         raise DimensionMismatch(f"matvec dimensions differ: {a.shape} x {len(v)}")
     _check_same_storage(a, v)
-    out = matvec_batched(a, v.data.reshape(1, -1), a.integer and v.integer)
-    return TropicalVector._wrap(a.kind, out.reshape(-1), a.integer and v.integer)
+    out = matvec_batched(a, v.data.reshape(1, -1), a.integer and v.integer, v_bound=v.abs_bound)
+    return TropicalVector._wrap(a.kind, out.reshape(-1), a.integer and v.integer, _sum_bound(a.abs_bound, v.abs_bound))
 
 
 @_on_operand_device
-def matvec_batched(a: TropicalMatrix, vs: "torch.Tensor | TropicalMatrix", integer: "bool | None" = None) -> torch.Tensor:
+def matvec_batched(a: TropicalMatrix, vs: "torch.Tensor | TropicalMatrix", integer: "bool | None" = None,
+                   v_bound: "float | None" = None) -> torch.Tensor:
     """Batched matvec: rows of ``vs`` (B x K, oriented storage of a's dtype)
     are B vectors; returns the B x M oriented results (one HBM pass over A
-    per 8 vectors)."""
+    per 8 vectors).  When a's and the vectors' magnitude bounds are known
+    (TropicalMatrix operands, or ``v_bound`` for a raw tensor) and prove that
+    no candidate can overflow, the kernels run without their screen."""
     if isinstance(vs, TropicalMatrix):
         _check_same_kind(a, vs)
         integer = a.integer and vs.integer if integer is None else integer
+        v_bound = vs.abs_bound
         vs = vs.data
     if integer is None:
         integer = a.integer
@@ -745,10 +780,11 @@ def matvec_batched(a: TropicalMatrix, vs: "torch.Tensor | TropicalMatrix", integ
     B = V.shape[0]
     out = torch.empty((B, a.n_rows), dtype=A.dtype, device=dev)
     flags = _flags.new(dev)
+    bound = _sum_bound(a.abs_bound, v_bound)
     _lib.call(
-        "btas_matvec", _dtype_code(A.dtype), _kind_code(a.kind), 1 if integer else 0,
+        "btas_matvec_bounded", _dtype_code(A.dtype), _kind_code(a.kind), 1 if integer else 0,
         _ptr(A), A.stride(0), a.n_rows, a.n_cols, _ptr(V), V.stride(0), B, _ptr(out), out.stride(0),
-        _ptr(flags), _stream(dev),
+        -1.0 if bound is None else bound, _ptr(flags), _stream(dev),
     )
     _flags.track(flags)
     return out

@@ -46,6 +46,33 @@ def test_matvec_batched_large(cuda, dtype):
                     assert out[b].tobytes() == want.tobytes(), (m, k, batch, b)
 
 
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_matvec_bound_selects_screen_free_path(cuda, dtype):
+    """Ingested operands carry their exact max |finite| (abs_bound); a bound
+    that proves no overflow runs the screen-free kernels, an unknown bound
+    (raw tensor, no v_bound) the screened ones — the same bytes either way,
+    for 1-4 vectors (matvec_kernel) and 5-8 (tensor-map wide kernel)."""
+    rng = np.random.default_rng(16)
+    m, k = 777, 4096
+    asym = rand_sym(rng, m, k, -1000, 1000, p_inf=0.1)
+    for kind in (MIN, MAX):
+        a = bt.TropicalMatrix(kind, asym, dtype=dtype)
+        assert a.abs_bound == float(np.abs(asym[np.isfinite(asym)]).max())
+        for batch in (1, 4, 8):
+            V = bt.TropicalMatrix(kind, rand_sym(rng, batch, k, -1000, 1000, p_inf=0.1), dtype=dtype)
+            bt.reset_saturation()
+            fast = bt.matvec_batched(a, V)  # bound known: screen-free
+            slow = bt.matvec_batched(a, V.data)  # bound unknown: screened
+            assert torch.equal(fast.view(torch.uint8), slow.view(torch.uint8)), (kind, batch)
+            assert not bt.saturation_seen()
+    # bounds propagate through products and ⊕ (|a (x) b| <= |a| + |b|)
+    b = bt.TropicalMatrix(MIN, rand_sym(rng, k, 64, -7, 9), dtype=dtype)
+    c = bt.matmul(bt.TropicalMatrix(MIN, asym, dtype=dtype), b)
+    assert c.abs_bound == a.abs_bound + b.abs_bound
+    assert float(np.abs(np.where(np.isfinite(c.to_numpy()), c.to_numpy(), 0)).max()) <= c.abs_bound
+    assert bt.ew_add(c, c).abs_bound == c.abs_bound and bt.identity_matrix(MIN, 3, dtype=dtype).abs_bound == 0.0
+
+
 def test_matvec_always_masks(cuda):
     """matvec masks overflow with no screen (matrix.py:408-420)."""
     for dtype, big, integer in ((torch.float64, 1e308, False), (torch.float32, 3e38, False),
