@@ -55,6 +55,12 @@ enum {
   BTAS_NUM_FLAGS = 8
 };
 
+/* btas_gemm_verify comparison modes (reference apsp.py:202-208) */
+enum {
+  BTAS_VERIFY_LE = 1, /* violation where !(Cref <= A (x) B): the triangle inequality d <= d (x) d */
+  BTAS_VERIFY_EQ = 2  /* violation where A (x) B != Cref: the closure fixpoint d (x) (I (+) A) = d */
+};
+
 /* GEMM kernel paths (bit index in BTAS_FLAG_PATH) */
 enum {
   BTAS_PATH_FAST32 = 0,  /* f32 FADD2+FMNMX3 / i32 VIADDMNMX */
@@ -162,6 +168,27 @@ int btas_gemm_peers(int dtype, int kind, int integer_mode,
                     const void* Cprev, int64_t ldcp, void* const* peer_C, int n_peers,
                     int32_t* dev_flags, void* workspace, size_t workspace_bytes,
                     btas_stream_t stream);
+
+/* The product A (x) B compared entry by entry with Cref in the GEMM
+ * epilogue, without storing it (the verifier's two products,
+ * find_apsp_violation apsp.py:202-208): *first_bad (caller-initialised to
+ * ~0) receives the smallest row-major index i*N + j that violates `mode`
+ * (atomicMin, so any tile order gives the reference's np.argmax answer) and
+ * BTAS_FLAG_CHANGED is set when any does.  Saturation behaves as btas_gemm.
+ * Min-plus only. */
+int btas_gemm_verify(int dtype, int kind, int integer_mode,
+                     const void* A, int64_t lda, const void* B, int64_t ldb,
+                     const void* Cref, int64_t ldcr, int64_t M, int64_t N, int64_t K,
+                     int mode, unsigned long long* first_bad,
+                     int32_t* dev_flags, void* workspace, size_t workspace_bytes,
+                     btas_stream_t stream);
+
+/* Elementwise half of find_apsp_violation (apsp.py:194-200) in one pass over
+ * D and the adjacency A (n x n, same storage): first[0] <- smallest i with
+ * D[i,i] != 0, first[1] <- smallest row-major index with !(D <= I (+) A)
+ * (atomicMin; first[] caller-initialised to ~0). */
+int btas_verify_base(int dtype, const void* D, int64_t ldd, const void* A, int64_t lda, int64_t n,
+                     unsigned long long* first, btas_stream_t stream);
 
 /* Measurement hooks (bench.py): when enabled, every btas_gemm brackets its
  * GEMM kernel launches (not the screen/packing) with CUDA events recorded on

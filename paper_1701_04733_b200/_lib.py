@@ -35,6 +35,7 @@ PATH_NAMES = {
     PATH_I32F64: "i32f64",
 }
 OK, ERR_INVALID, ERR_CUDA, ERR_WORKSPACE, ERR_UNSUPPORTED = 0, 1, 2, 3, 4
+VERIFY_LE, VERIFY_EQ = 1, 2
 APSP_SMALL_MAX_N = 1024
 
 
@@ -109,6 +110,11 @@ SIGNATURES = {
         [_i32, _i32, _i32, _p, _i64, _p, _i64, _p, _i64, _i64, _i64, _i64, _p, _i64, ctypes.POINTER(_p), _i32, _p, _p,
          _sz, _p],
     ),
+    "btas_gemm_verify": (
+        _i32,
+        [_i32, _i32, _i32, _p, _i64, _p, _i64, _p, _i64, _i64, _i64, _i64, _i32, _p, _p, _p, _sz, _p],
+    ),
+    "btas_verify_base": (_i32, [_i32, _p, _i64, _p, _i64, _i64, _p, _p]),
     "btas_gemm_timing": (_i32, [_i32]),
     "btas_gemm_timing_read": (_i32, [ctypes.POINTER(_dbl), ctypes.POINTER(_i32)]),
     "btas_matvec": (_i32, [_i32, _i32, _i32, _p, _i64, _i64, _i64, _p, _i64, _i64, _p, _i64, _p, _p]),

@@ -829,6 +829,51 @@ extern "C" int btas_diag_negative(int dtype, const void* d, int64_t ld, int64_t 
   return BTAS_OK;
 }
 
+// ------------------------------------------------------------------ verifier (elementwise half)
+// find_apsp_violation's first two checks (apsp.py:194-200) in one pass:
+// first[0] = smallest i with D[i,i] != 0, first[1] = smallest row-major index
+// with !(D[i,j] <= base[i,j]) where base = I (+) A (diagonal min(A_ii, 0)).
+// One CTA row per grid step, threads along the row (coalesced), four loads
+// in flight per thread; atomics only on violations.
+template <class T>
+__global__ void __launch_bounds__(256) verify_base_kernel(const T* __restrict__ D, int64_t ldd,
+                                                          const T* __restrict__ A, int64_t lda, int64_t n,
+                                                          unsigned long long* first) {
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const T* drow = D + i * ldd;
+    const T* arow = A + i * lda;
+    auto check = [&](int64_t j, T d, T a) {
+      if (j == i) {
+        if (d != (T)0) atomicMin(&first[0], (unsigned long long)i);
+        a = a < (T)0 ? a : (T)0;
+      }
+      if (!(d <= a)) atomicMin(&first[1], (unsigned long long)(i * n + j));
+    };
+    int64_t j = threadIdx.x;
+    for (; j + 3 * 256 < n; j += 4 * 256) {
+      T d[4], a[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        d[u] = drow[j + u * 256];
+        a[u] = arow[j + u * 256];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) check(j + u * 256, d[u], a[u]);
+    }
+    for (; j < n; j += 256) check(j, drow[j], arow[j]);
+  }
+}
+
+extern "C" int btas_verify_base(int dtype, const void* D, int64_t ldd, const void* A, int64_t lda, int64_t n,
+                                unsigned long long* first, btas_stream_t stream) {
+  if (!D || !A || !first || n < 1 || ldd < n || lda < n || !valid_dtype(dtype)) return BTAS_ERR_INVALID;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const unsigned grid = (unsigned)std::min<int64_t>(n, (int64_t)device_sm_count() * 8);
+  BTAS_DISPATCH(dtype, verify_base_kernel<T><<<grid, 256, 0, st>>>((const T*)D, ldd, (const T*)A, lda, n, first))
+  BTAS_CUDA_CHECK_LAUNCH();
+  return BTAS_OK;
+}
+
 extern "C" int btas_matvec_bounded(int dtype, int kind, int integer_mode, const void* A, int64_t lda, int64_t M,
                                    int64_t K, const void* V, int64_t ldv, int64_t batch, void* Out, int64_t ldo,
                                    double abs_bound, int32_t* flags, btas_stream_t stream) {

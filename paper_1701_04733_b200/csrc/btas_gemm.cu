@@ -100,10 +100,11 @@ extern "C" size_t btas_gemm_workspace_bytes(int dtype, int64_t M, int64_t N, int
 static int gemm_entry(int dtype, int kind, int integer_mode, const void* A, int64_t lda, const void* B, int64_t ldb,
                       const void* Z, int64_t ldz, void* C, int64_t ldc, int64_t M, int64_t N, int64_t K,
                       const void* Cprev, int64_t ldcp, int32_t* dev_flags, void* workspace, size_t workspace_bytes,
-                      void* const* peers, int n_peers, btas_stream_t stream) {
-  if (n_peers < 0 || n_peers > kMaxPeers || (n_peers > 0 && !peers)) return BTAS_ERR_INVALID;
+                      const GemmExtras& x, btas_stream_t stream) {
+  const int n_peers = x.n_peers;
+  if (n_peers < 0 || n_peers > kMaxPeers || (n_peers > 0 && !x.peers)) return BTAS_ERR_INVALID;
   for (int q = 0; q < n_peers; ++q)
-    if (!peers[q]) return BTAS_ERR_INVALID;
+    if (!x.peers[q]) return BTAS_ERR_INVALID;
   if (!A || !B || !C || !dev_flags || !workspace) return BTAS_ERR_INVALID;
   if (M < 1 || N < 1 || K < 1 || lda < K || ldb < N || ldc < N) return BTAS_ERR_INVALID;
   if (Z && ldz < N) return BTAS_ERR_INVALID;
@@ -118,13 +119,13 @@ static int gemm_entry(int dtype, int kind, int integer_mode, const void* A, int6
   switch (dtype) {
     case BTAS_F32:
       return gemm_f32(mn, integer_mode, (const float*)A, lda, (const float*)B, ldb, (const float*)Z, ldz, (float*)C,
-                      ldc, M, N, K, (const float*)Cprev, ldcp, dev_flags, ws, peers, n_peers, st);
+                      ldc, M, N, K, (const float*)Cprev, ldcp, dev_flags, ws, x, st);
     case BTAS_I32:
       return gemm_i32(mn, integer_mode, (const int32_t*)A, lda, (const int32_t*)B, ldb, (const int32_t*)Z, ldz,
-                      (int32_t*)C, ldc, M, N, K, (const int32_t*)Cprev, ldcp, dev_flags, ws, peers, n_peers, st);
+                      (int32_t*)C, ldc, M, N, K, (const int32_t*)Cprev, ldcp, dev_flags, ws, x, st);
     default:
       return gemm_f64(mn, integer_mode, (const double*)A, lda, (const double*)B, ldb, (const double*)Z, ldz,
-                      (double*)C, ldc, M, N, K, (const double*)Cprev, ldcp, dev_flags, ws, peers, n_peers, st);
+                      (double*)C, ldc, M, N, K, (const double*)Cprev, ldcp, dev_flags, ws, x, st);
   }
 }
 
@@ -133,13 +134,31 @@ extern "C" int btas_gemm(int dtype, int kind, int integer_mode, const void* A, i
                          int64_t K, const void* Cprev, int64_t ldcp, int32_t* dev_flags, void* workspace,
                          size_t workspace_bytes, btas_stream_t stream) {
   return gemm_entry(dtype, kind, integer_mode, A, lda, B, ldb, Z, ldz, C, ldc, M, N, K, Cprev, ldcp, dev_flags,
-                    workspace, workspace_bytes, nullptr, 0, stream);
+                    workspace, workspace_bytes, GemmExtras{}, stream);
+}
+
+extern "C" int btas_gemm_verify(int dtype, int kind, int integer_mode, const void* A, int64_t lda, const void* B,
+                                int64_t ldb, const void* Cref, int64_t ldcr, int64_t M, int64_t N, int64_t K, int mode,
+                                unsigned long long* first_bad, int32_t* dev_flags, void* workspace,
+                                size_t workspace_bytes, btas_stream_t stream) {
+  if (!Cref || !first_bad || kind != BTAS_MIN_PLUS || (mode != BTAS_VERIFY_LE && mode != BTAS_VERIFY_EQ))
+    return BTAS_ERR_INVALID;
+  GemmExtras x;
+  x.first_bad = first_bad;
+  x.verify_mode = mode;
+  // C is never written by the verifier kernels; Cref stands in for the
+  // pointer argument checks
+  return gemm_entry(dtype, kind, integer_mode, A, lda, B, ldb, nullptr, 0, const_cast<void*>(Cref), ldcr, M, N, K,
+                    Cref, ldcr, dev_flags, workspace, workspace_bytes, x, stream);
 }
 
 extern "C" int btas_gemm_peers(int dtype, int kind, int integer_mode, const void* A, int64_t lda, const void* B,
                                int64_t ldb, void* C, int64_t ldc, int64_t M, int64_t N, int64_t K, const void* Cprev,
                                int64_t ldcp, void* const* peer_C, int n_peers, int32_t* dev_flags, void* workspace,
                                size_t workspace_bytes, btas_stream_t stream) {
+  GemmExtras x;
+  x.peers = peer_C;
+  x.n_peers = n_peers;
   return gemm_entry(dtype, kind, integer_mode, A, lda, B, ldb, nullptr, 0, C, ldc, M, N, K, Cprev, ldcp, dev_flags,
-                    workspace, workspace_bytes, peer_C, n_peers, stream);
+                    workspace, workspace_bytes, x, stream);
 }

@@ -66,6 +66,18 @@ struct GemmArgs {
   int n_peers;
   int integer_mode;
   double limit;          // saturation limit (integer limit, or +inf for float mode)
+  // verifier products (btas_gemm_verify): compare with Cprev instead of
+  // storing C; smallest violating row-major index -> *first_bad
+  unsigned long long* first_bad;
+  int verify_mode;       // BTAS_VERIFY_LE / BTAS_VERIFY_EQ
+};
+
+// per-call options of the btas_gemm drivers beyond the plain product
+struct GemmExtras {
+  void* const* peers = nullptr;  // fused all-gather targets (btas_gemm_peers)
+  int n_peers = 0;
+  unsigned long long* first_bad = nullptr;  // verifier product (btas_gemm_verify)
+  int verify_mode = 0;
 };
 
 // ---------------------------------------------------------------------------
@@ -339,7 +351,19 @@ struct GemmShape {
 // bit 1 = fixpoint reference Cprev present.  Separate instantiations keep the
 // plain product's epilogue minimal (measured: a generic epilogue costs the
 // n = 16384 GEMM ~1 %, profiles/r01_experiments.md).
-enum { kEpiPlain = 0, kEpiAcc = 1, kEpiCmp = 2, kEpiBoth = 3, kEpiPeers = 4 };
+// bit 2 = peer stores (fused all-gather); bit 3 = verify (compare with
+// Cprev under g.verify_mode, record the first violating index, no store).
+enum { kEpiPlain = 0, kEpiAcc = 1, kEpiCmp = 2, kEpiBoth = 3, kEpiPeers = 4, kEpiVerify = 8 };
+
+// verifier epilogue: one output entry against the reference value
+template <class Out>
+BTAS_D void verify_entry(const GemmArgs& g, Out v, Out ref, int64_t row, int64_t col, bool& bad_any) {
+  const bool bad = g.verify_mode == BTAS_VERIFY_LE ? !(ref <= v) : (v != ref);
+  if (bad) {
+    bad_any = true;
+    atomicMin(g.first_bad, (unsigned long long)(row * g.N + col));
+  }
+}
 constexpr int kMaxPeers = 7;
 
 template <class P, bool MIN, int EPI>
@@ -498,12 +522,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
               v[c] = P::finish(acc[i][r][j][c], g);
               if (Z != nullptr) v[c] = combine<Out, MIN>(v[c], xi[i][r][j][c]);
             }
-            if (Cp != nullptr) changed |= bits_differ(v[0], xi[i][r][j][0]) | bits_differ(v[1], xi[i][r][j][1]);
-            if (diag_tile) diag_neg |= (row == col0 && v[0] < (Out)0) | (row == col0 + 1 && v[1] < (Out)0);
-            st2(C + row * g.ldc + col0, v);
-            if constexpr ((EPI & kEpiPeers) != 0) {
+            if constexpr ((EPI & kEpiVerify) != 0) {
+              verify_entry(g, v[0], xi[i][r][j][0], row, col0, changed);
+              verify_entry(g, v[1], xi[i][r][j][1], row, col0 + 1, changed);
+            } else {
+              if (Cp != nullptr) changed |= bits_differ(v[0], xi[i][r][j][0]) | bits_differ(v[1], xi[i][r][j][1]);
+              if (diag_tile) diag_neg |= (row == col0 && v[0] < (Out)0) | (row == col0 + 1 && v[1] < (Out)0);
+              st2(C + row * g.ldc + col0, v);
+              if constexpr ((EPI & kEpiPeers) != 0) {
 #pragma unroll 1
-              for (int q = 0; q < g.n_peers; ++q) st2(static_cast<Out*>(g.peer_C[q]) + row * g.ldc + col0, v);
+                for (int q = 0; q < g.n_peers; ++q) st2(static_cast<Out*>(g.peer_C[q]) + row * g.ldc + col0, v);
+              }
             }
           }
         }
@@ -543,6 +572,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
           for (int c = 0; c < 2; ++c) {
             v[c] = P::finish(acc[i][r][j][c], g);
             if (Z != nullptr) v[c] = combine<Out, MIN>(v[c], xv[i][r][j][c]);
+          }
+          if constexpr ((EPI & kEpiVerify) != 0) {
+            if (col0 < g.N) verify_entry(g, v[0], xv[i][r][j][0], row, col0, changed);
+            if (col0 + 1 < g.N) verify_entry(g, v[1], xv[i][r][j][1], row, col0 + 1, changed);
+            continue;
           }
           if (Cp != nullptr && Z == nullptr) {
             if (col0 < g.N) changed |= bits_differ(v[0], xv[i][r][j][0]);
@@ -605,6 +639,14 @@ int launch_gemm_epi(const GemmArgs& g, cudaStream_t stream) {
 
 template <class P, bool MIN>
 int launch_tropical_gemm(const GemmArgs& g, cudaStream_t stream) {
+  if (g.first_bad != nullptr) {  // verifier product: min-plus, compare only
+    if constexpr (MIN) {
+      if (g.Cprev == nullptr || g.Z != nullptr || g.n_peers > 0) return BTAS_ERR_INVALID;
+      return launch_gemm_epi<P, MIN, kEpiCmp | kEpiVerify>(g, stream);
+    } else {
+      return BTAS_ERR_UNSUPPORTED;
+    }
+  }
   const int epi = (g.Z != nullptr ? kEpiAcc : 0) | (g.Cprev != nullptr ? kEpiCmp : 0);
   if (g.n_peers > 0) {
     // peer-store variants: the squaring step (compare against Cprev) and the plain product

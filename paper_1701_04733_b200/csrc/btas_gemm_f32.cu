@@ -5,10 +5,10 @@ namespace btas {
 
 BTAS_GEMM_DRIVER_DECL(float, gemm_f32) {
   if (!min_plus) return gemm_f32_max(integer_mode, A, lda, B, ldb, Z, ldz, C, ldc, M, N, K, Cprev, ldcp, flags, ws,
-                                     peers, n_peers, st);
+                                     x, st);
   const gemm_impl::WsLayout L = gemm_impl::ws_layout(Traits<float>::dtype, M, N, K);
   return gemm_impl::gemm_typed<float, true>(integer_mode, A, lda, B, ldb, Z, ldz, C, ldc, M, N, K, Cprev, ldcp, flags, ws,
-                                         L, peers, n_peers, st);
+                                         L, x, st);
 }
 
 size_t gemm_ws_total(int dtype, int64_t M, int64_t N, int64_t K) {

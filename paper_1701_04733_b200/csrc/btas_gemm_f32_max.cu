@@ -6,7 +6,7 @@ namespace btas {
 BTAS_GEMM_HALF_DECL(float, gemm_f32_max) {
   const gemm_impl::WsLayout L = gemm_impl::ws_layout(Traits<float>::dtype, M, N, K);
   return gemm_impl::gemm_typed<float, false>(integer_mode, A, lda, B, ldb, Z, ldz, C, ldc, M, N, K, Cprev, ldcp, flags,
-                                          ws, L, peers, n_peers, st);
+                                          ws, L, x, st);
 }
 
 }  // namespace btas

@@ -5,10 +5,10 @@ namespace btas {
 
 BTAS_GEMM_DRIVER_DECL(double, gemm_f64) {
   if (!min_plus) return gemm_f64_max(integer_mode, A, lda, B, ldb, Z, ldz, C, ldc, M, N, K, Cprev, ldcp, flags, ws,
-                                     peers, n_peers, st);
+                                     x, st);
   const gemm_impl::WsLayout L = gemm_impl::ws_layout(Traits<double>::dtype, M, N, K);
   return gemm_impl::gemm_typed<double, true>(integer_mode, A, lda, B, ldb, Z, ldz, C, ldc, M, N, K, Cprev, ldcp, flags, ws,
-                                         L, peers, n_peers, st);
+                                         L, x, st);
 }
 
 }  // namespace btas

@@ -5,10 +5,10 @@ namespace btas {
 
 BTAS_GEMM_DRIVER_DECL(int32_t, gemm_i32) {
   if (!min_plus) return gemm_i32_max(integer_mode, A, lda, B, ldb, Z, ldz, C, ldc, M, N, K, Cprev, ldcp, flags, ws,
-                                     peers, n_peers, st);
+                                     x, st);
   const gemm_impl::WsLayout L = gemm_impl::ws_layout(Traits<int32_t>::dtype, M, N, K);
   return gemm_impl::gemm_typed<int32_t, true>(integer_mode, A, lda, B, ldb, Z, ldz, C, ldc, M, N, K, Cprev, ldcp, flags, ws,
-                                         L, peers, n_peers, st);
+                                         L, x, st);
 }
 
 }  // namespace btas

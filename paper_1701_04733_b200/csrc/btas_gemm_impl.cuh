@@ -326,7 +326,9 @@ __global__ void pack_b_kernel(const T* __restrict__ B, int64_t ldb, int64_t K, i
 template <class T, bool MIN>
 int gemm_typed(int integer_mode, const T* A, int64_t lda, const T* B, int64_t ldb, const T* Z, int64_t ldz, T* C,
                int64_t ldc, int64_t M, int64_t N, int64_t K, const T* Cprev, int64_t ldcp, int32_t* flags,
-               unsigned char* ws, const WsLayout& L, void* const* peers, int n_peers, cudaStream_t st) {
+               unsigned char* ws, const WsLayout& L, const GemmExtras& x, cudaStream_t st) {
+  void* const* peers = x.peers;
+  const int n_peers = x.n_peers;
   using G = GemmGeometry<T>;
   constexpr bool kIsF64 = Traits<T>::dtype == BTAS_F64;
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(ws + L.ctrl);
@@ -382,6 +384,8 @@ int gemm_typed(int integer_mode, const T* A, int64_t lda, const T* B, int64_t ld
     g.limit = int_mode ? limit : INFINITY;
     g.n_peers = n_peers;
     for (int q = 0; q < n_peers && q < kMaxPeers; ++q) g.peer_C[q] = peers[q];
+    g.first_bad = x.first_bad;
+    g.verify_mode = x.verify_mode;
   }
   GemmArgs g32{};  // float64 integer operands through the int32 kernel
   if constexpr (kIsF64) {
@@ -470,7 +474,7 @@ int gemm_typed(int integer_mode, const T* A, int64_t lda, const T* B, int64_t ld
 #define BTAS_GEMM_DRIVER_DECL(T, NAME)                                                                       \
   int NAME(bool min_plus, int integer_mode, const T* A, int64_t lda, const T* B, int64_t ldb, const T* Z,      \
            int64_t ldz, T* C, int64_t ldc, int64_t M, int64_t N, int64_t K, const T* Cprev, int64_t ldcp,      \
-           int32_t* flags, unsigned char* ws, void* const* peers, int n_peers, cudaStream_t st)
+           int32_t* flags, unsigned char* ws, const GemmExtras& x, cudaStream_t st)
 BTAS_GEMM_DRIVER_DECL(float, gemm_f32);
 BTAS_GEMM_DRIVER_DECL(int32_t, gemm_i32);
 BTAS_GEMM_DRIVER_DECL(double, gemm_f64);
@@ -479,7 +483,7 @@ BTAS_GEMM_DRIVER_DECL(double, gemm_f64);
 #define BTAS_GEMM_HALF_DECL(T, NAME)                                                                          \
   int NAME(int integer_mode, const T* A, int64_t lda, const T* B, int64_t ldb, const T* Z, int64_t ldz, T* C,    \
            int64_t ldc, int64_t M, int64_t N, int64_t K, const T* Cprev, int64_t ldcp, int32_t* flags,         \
-           unsigned char* ws, void* const* peers, int n_peers, cudaStream_t st)
+           unsigned char* ws, const GemmExtras& x, cudaStream_t st)
 BTAS_GEMM_HALF_DECL(float, gemm_f32_max);
 BTAS_GEMM_HALF_DECL(int32_t, gemm_i32_max);
 BTAS_GEMM_HALF_DECL(double, gemm_f64_max);

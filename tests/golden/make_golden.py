@@ -290,6 +290,57 @@ def kat_cases():
     np.savez_compressed(HERE / "kat.npz", **arrays)
 
 
+def verify_cases():
+    """find_apsp_violation (apsp.py:181-210) on correct and deliberately
+    broken distance matrices (0x5EF1): the reference's exact messages
+    (None -> ""), including its acceptance of too-small fixpoints (SURVEY
+    §9 quirk 2: the all-zero matrix)."""
+    rng = np.random.default_rng(0x5EF1)
+    arrays = {}
+    msgs = []
+    case = 0
+
+    def add(adj, d):
+        nonlocal case
+        a = ref.TropicalMatrix(MIN, np.where(np.isinf(adj), INF, adj))
+        dm = ref.DistanceMatrix(d.shape[0], ref.TropicalMatrix(MIN, np.where(np.isinf(d), INF, d)))
+        msgs.append(ref.find_apsp_violation(a, dm) or "")
+        arrays[f"adj{case}"] = compact(a.data)
+        arrays[f"d{case}"] = compact(dm.dist.data)
+        case += 1
+
+    for n in (1, 2, 3, 5, 8, 13, 24, 40, 64, 130):
+        for lo in (0, -3):
+            adj = rng.integers(lo, 20, (n, n)).astype(np.float64)
+            adj[rng.random((n, n)) < 0.6] = INF
+            np.fill_diagonal(adj, np.where(rng.random(n) < 0.3, rng.integers(0, 5, n), 0).astype(float))
+            a = ref.TropicalMatrix(MIN, np.where(np.isinf(adj), INF, adj))
+            rep = ref.floyd_warshall(a)
+            if rep.negative_cycle:
+                continue
+            d = np.array(rep.distances.dist.data)
+            base = np.array(adj)
+            np.fill_diagonal(base, np.minimum(np.diagonal(base), 0.0))
+            add(adj, d)  # correct
+            add(adj, np.zeros((n, n)))  # too small, accepted when the weights are non-negative
+            add(adj, base)  # the closure base: triangle / fixpoint failures past 1 hop
+            i, j = rng.integers(0, n, 2)
+            x = d.copy(); x[i, i] = float(rng.integers(1, 9)); add(adj, x)  # nonzero diagonal
+            x = d.copy(); x[i, i] = INF; add(adj, x)
+            fin = np.argwhere(np.isfinite(base) & ~np.eye(n, dtype=bool))
+            if len(fin):
+                r, c = fin[rng.integers(len(fin))]
+                x = d.copy(); x[r, c] = base[r, c] + 1.0; add(adj, x)  # exceeds the edge
+                x = d.copy(); x[r, c] = INF; add(adj, x)
+            fin = np.argwhere(np.isfinite(d) & ~np.eye(n, dtype=bool))
+            if len(fin):
+                r, c = fin[rng.integers(len(fin))]
+                x = d.copy(); x[r, c] -= 1.0; add(adj, x)  # too small by one somewhere
+                x = d.copy(); x[r, :] = np.minimum(x[r, :], 0.0); x[r, r] = 0.0; add(adj, x)
+    arrays["msg"] = np.array(msgs)
+    np.savez_compressed(HERE / "verify.npz", **arrays)
+
+
 def main():
     gemm_cases(0x04AC1E, 200, lambda c: MIN if c % 3 else MAX, "gemm_acceptance.npz")
     gemm_cases(0xB7A5, 120, lambda c: MIN if c % 2 else MAX, "gemm_matrix.npz")
@@ -301,9 +352,13 @@ def main():
     generator_families()
     edgelist_cases()
     kat_cases()
+    verify_cases()
     for f in sorted(HERE.glob("*.npz")):
         print(f"{f.name}: {f.stat().st_size / 1024:.1f} KiB")
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["verify"]:  # only the verifier fixture
+        verify_cases()
+    else:
+        main()

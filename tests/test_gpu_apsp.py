@@ -186,6 +186,49 @@ def test_verifier(cuda):
     assert "edge" in bt.find_apsp_violation(three, bt.DistanceMatrix.from_matrix(bt.TropicalMatrix(MIN, above)))
 
 
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_verifier_messages_match_reference(cuda, golden, dtype):
+    """The fused verifier (btas_verify_base + two btas_gemm_verify products)
+    returns the reference's find_apsp_violation message — check order, first
+    offending index and numpy-scalar value repr — on correct, too-small
+    (accepted) and deliberately broken distance matrices
+    (tests/golden/verify.npz, made by the reference)."""
+    g = golden("verify.npz")
+    msgs = g["msg"]
+    for case in range(len(msgs)):
+        adj = bt.TropicalMatrix(MIN, symbolic(g[f"adj{case}"]), dtype=dtype)
+        d = bt.DistanceMatrix.from_matrix(bt.TropicalMatrix(MIN, symbolic(g[f"d{case}"]), dtype=dtype))
+        got = bt.find_apsp_violation(adj, d)
+        assert (got or "") == str(msgs[case]), case
+        assert bt.verify_apsp(adj, d) == (str(msgs[case]) == "")
+
+
+def test_verifier_at_c3_scale(cuda):
+    """The verifier at n = 32768 (int32): accepts the true distances, and
+    names the exact first violation of a broken diagonal, an entry above its
+    edge and an entry above a shorter path."""
+    n = 32768
+    adj = random_graph_matrix(n, 0.5, (1, 100), instance_seed(1, n), dtype=torch.int32)
+    d = bt.floyd_warshall(adj).distances.dist
+    assert bt.find_apsp_violation(adj, bt.DistanceMatrix(n, d)) is None
+
+    def broken(i, j, v):
+        data = d.data.clone()
+        data[i, j] = v
+        return bt.DistanceMatrix(n, bt.TropicalMatrix._wrap(MIN, data, True))
+
+    assert bt.find_apsp_violation(adj, broken(777, 777, 1)) == "diagonal entry (777,777) is np.float64(1.0), expected 0"
+    a = adj.data
+    r = 20001
+    c = int(torch.nonzero(a[r] < (1 << 28))[5].item())
+    assert bt.find_apsp_violation(adj, broken(r, c, int(a[r, c]) + 1)) == \
+        f"distance ({r},{c}) exceeds the direct edge weight"
+    # an entry raised above its true distance but not above its edge
+    cols = torch.nonzero((a[r] < (1 << 28)) & (a[r] > d.data[r] + 1)).reshape(-1)
+    c = int(cols[0].item())
+    assert bt.find_apsp_violation(adj, broken(r, c, int(d.data[r, c]) + 1)) == f"triangle inequality fails at ({r},{c})"
+
+
 def test_input_errors(cuda):
     rect = bt.TropicalMatrix(MIN, [[0, 1, 2], [3, 0, 4]])
     wrong = bt.TropicalMatrix(MAX, [[0]])
