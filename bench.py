@@ -781,21 +781,27 @@ def apsp_arm(args, rank, world, dev):
     for _ in range(max(3, args.warmup)):
         rep = solver(adj)
     torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rep = solver(adj)
+    torch.cuda.synchronize()
+    # small solves (C1: 0.2 ms) repeat until the timed region spans >= 1.5 s
+    # so the clock sampler sees it; the same count on every rank
+    steps = int(_max_over_ranks(max(args.steps, math.ceil(1.5 / max(time.perf_counter() - t0, 1e-5))), world, dev))
     if world > 1:
         dist.barrier()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev.index, period_ms=50) as clocks:
         s.record()
-        for _ in range(args.steps):
+        for _ in range(steps):
             rep = solver(adj)
         e.record()
         torch.cuda.synchronize()
-    ms = _max_over_ranks(s.elapsed_time(e) / args.steps, world, dev)
+    ms = _max_over_ranks(s.elapsed_time(e) / steps, world, dev)
     clk = clocks.summary()
     mults = rep.multiplications_performed
     pairs = float(n) ** 3 * (1 if args.workload == "fw" else mults)
-    res = {"metric": f"APSP time n={n}", "value": round(ms / 1e3, 4), "unit": "s", "n_gpus": world,
-           "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms, 3), "higher_is_better": False,
+    res = {"metric": f"APSP time n={n}", "value": round(ms / 1e3, 6), "unit": "s", "n_gpus": world,
+           "steps": steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms, 3), "higher_is_better": False,
            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
            "dtype": "i32" if dtype == torch.int32 else "f32",
            "data": "synthetic",
