@@ -633,14 +633,18 @@ int matvec_launch(int int_mode, const T* A, int64_t lda, int64_t M, int64_t K, c
         continue;
       }
     }
+    // 1-4 vectors: the screened kernel even when a bound proves the screen
+    // moot — ptxas schedules the screen-free instantiation with fewer loads
+    // in flight (measured 4.6 vs 6.4 TB/s at 4 vectors, tools/matvec_ab.py);
+    // at <= 4 add-min pairs per A element the screen is free anyway
     if (nb == 1) {
-      matvec_kernel<T, MIN, 16, 1, SCREEN><<<(unsigned)ceil_div(M, 16), 256, 0, st>>>(A, lda, M, K, Vb, ldv, nb, Ob, ldo,
+      matvec_kernel<T, MIN, 16, 1, true><<<(unsigned)ceil_div(M, 16), 256, 0, st>>>(A, lda, M, K, Vb, ldv, nb, Ob, ldo,
                                                                             int_mode, limit, flags);
     } else if (nb <= 2) {
-      matvec_kernel<T, MIN, 8, 2, SCREEN><<<(unsigned)ceil_div(M, 8), 256, 0, st>>>(A, lda, M, K, Vb, ldv, nb, Ob, ldo,
+      matvec_kernel<T, MIN, 8, 2, true><<<(unsigned)ceil_div(M, 8), 256, 0, st>>>(A, lda, M, K, Vb, ldv, nb, Ob, ldo,
                                                                           int_mode, limit, flags);
     } else if (nb <= 4) {
-      matvec_kernel<T, MIN, 8, 4, SCREEN><<<(unsigned)ceil_div(M, 8), 256, 0, st>>>(A, lda, M, K, Vb, ldv, nb, Ob, ldo,
+      matvec_kernel<T, MIN, 8, 4, true><<<(unsigned)ceil_div(M, 8), 256, 0, st>>>(A, lda, M, K, Vb, ldv, nb, Ob, ldo,
                                                                           int_mode, limit, flags);
     }
     BTAS_CUDA_CHECK_LAUNCH();

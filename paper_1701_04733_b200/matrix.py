@@ -774,20 +774,24 @@ def matvec_batched(a: TropicalMatrix, vs: "torch.Tensor | TropicalMatrix", integ
         raise DimensionMismatch(f"batched matvec needs B x {a.n_cols} vectors, got {tuple(vs.shape)}")
     if vs.dtype != a.dtype:
         raise DtypeMismatch(f"mixed storage dtypes: {a.dtype} vs {vs.dtype}")
-    A = _rowmajor(a.data)
-    V = _rowmajor(vs)
+    out, _ = _matvec(_rowmajor(a.data), _rowmajor(vs), a.kind, integer, _sum_bound(a.abs_bound, v_bound))
+    return out
+
+
+def _matvec(A: torch.Tensor, V: torch.Tensor, kind: SemiringKind, integer: bool,
+            bound: "float | None") -> "tuple[torch.Tensor, torch.Tensor]":
+    """One btas_matvec_bounded call on the current stream: (B x M result,
+    flag words)."""
     dev = A.device
-    B = V.shape[0]
-    out = torch.empty((B, a.n_rows), dtype=A.dtype, device=dev)
+    out = torch.empty((V.shape[0], A.shape[0]), dtype=A.dtype, device=dev)
     flags = _flags.new(dev)
-    bound = _sum_bound(a.abs_bound, v_bound)
     _lib.call(
-        "btas_matvec_bounded", _dtype_code(A.dtype), _kind_code(a.kind), 1 if integer else 0,
-        _ptr(A), A.stride(0), a.n_rows, a.n_cols, _ptr(V), V.stride(0), B, _ptr(out), out.stride(0),
+        "btas_matvec_bounded", _dtype_code(A.dtype), _kind_code(kind), 1 if integer else 0,
+        _ptr(A), A.stride(0), A.shape[0], A.shape[1], _ptr(V), V.stride(0), V.shape[0], _ptr(out), out.stride(0),
         -1.0 if bound is None else bound, _ptr(flags), _stream(dev),
     )
     _flags.track(flags)
-    return out
+    return out, flags
 
 
 @_on_operand_device

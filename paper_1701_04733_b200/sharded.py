@@ -112,15 +112,15 @@ def _diag_rows(d_rows: torch.Tensor, r0: int) -> torch.Tensor:
     return (diag < 0).any().to(torch.int32)
 
 
-def _peer_buffers(shape, dtype, dev, group, world):
-    """Two symmetric-memory buffers and, per buffer, the base addresses of
-    the other ranks' copies; None when symmetric memory is unavailable."""
+def _peer_buffers(shape, dtype, dev, group, world, count=2):
+    """``count`` symmetric-memory buffers and, per buffer, the base addresses
+    of the other ranks' copies; None when symmetric memory is unavailable."""
     try:
         import torch.distributed._symmetric_memory as symm_mem
 
         bufs, ptrs = [], []
         me = dist.get_rank(group)
-        for _ in range(2):
+        for _ in range(count):
             t = symm_mem.empty(*shape, dtype=dtype, device=dev)
             h = symm_mem.rendezvous(t, group if group is not None else dist.group.WORLD)
             addrs = [int(a) for a in h.buffer_ptrs]
@@ -299,6 +299,129 @@ def apsp_by_squaring_emulated(adj, world: int):
     rep = ApspReport(distances=DistanceMatrix(n, dist_m), algorithm=Algorithm.REPEATED_SQUARING,
                      negative_cycle=negative, multiplications_performed=mults)
     return rep, per_rank
+
+
+# ---------------------------------------------------------------------------
+# row-sharded matmul / matvec (GEMM and matvec rows)
+# ---------------------------------------------------------------------------
+def _cuda_gemm_plain(kind, integer: bool) -> Callable:
+    from .matrix import _gemm
+
+    def gemm_rows(a_rows, b, out, z_rows=None, peers=None):
+        _, flags = _gemm(a_rows, b, kind, integer, out=out, z=z_rows, peers=peers)
+        return flags[_lib.FLAG_SATURATED].reshape(1).to(torch.int32)
+
+    return gemm_rows
+
+
+def matmul_sharded(x: torch.Tensor, y: torch.Tensor, kind, integer: bool, z: "torch.Tensor | None" = None,
+                   group=None, gemm_rows: "Callable | None" = None, align: int = 128,
+                   peer_buffers: "Callable | None" = None) -> "tuple[torch.Tensor, bool]":
+    """Rows of ``x ⊗ y [⊕ z]`` (oriented storage, the same operands on every
+    rank) split over the ranks of ``group``: rank r computes rows
+    [r*chunk, (r+1)*chunk) against the replicated ``y`` and every rank ends
+    with the full product.  Rows are independent (k is never split), so the
+    product is byte-identical to the single-GPU matmul for any P.  On NCCL
+    groups with symmetric memory the exchange is fused into the GEMM
+    epilogue (peer stores of each finished tile into every rank's copy);
+    otherwise NCCL all_gather.  Returns (product, saturated on any rank)."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    m, n = x.shape[0], y.shape[1]
+    dev = x.device
+    fused_ok = gemm_rows is None and z is None and _want_peer_exchange(group, world, dev)
+    gemm_rows = gemm_rows or _cuda_gemm_plain(kind, integer)
+    chunk, spans = partition(m, world, align)
+    r0, r1 = spans[rank]
+    peer = (peer_buffers or _peer_buffers)((world * chunk, n), x.dtype, dev, group, world, 1) if fused_ok else None
+    if fused_ok:  # every rank must take the same exchange
+        ok = torch.tensor([1 if peer is not None else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if not int(_host_read(ok)[0]):
+            peer = None
+    if peer is not None:
+        bufs, peer_ptrs = peer
+        full = bufs[0]
+        peers = [a + r0 * n * x.element_size() for a in peer_ptrs[0]]
+        sat = gemm_rows(x[r0:r1], y, full[r0:r1], peers=peers) if r1 > r0 else \
+            torch.zeros(1, dtype=torch.int32, device=dev)
+    else:
+        full = torch.empty((world * chunk, n), dtype=x.dtype, device=dev)
+        sat = gemm_rows(x[r0:r1], y, full[r0:r1], z_rows=None if z is None else z[r0:r1]) if r1 > r0 else \
+            torch.zeros(1, dtype=torch.int32, device=dev)
+        dist.all_gather_into_tensor(full, full[rank * chunk : (rank + 1) * chunk], group=group)
+    # the flag all-reduce doubles as the barrier after the peers' stores
+    sat = sat.to(torch.int32).reshape(1).clone()
+    dist.all_reduce(sat, op=dist.ReduceOp.MAX, group=group)
+    saturated = bool(int(_host_read(sat)[0]))
+    out = full[:m]
+    return (out if world * chunk == m and peer is None else out.clone()), saturated
+
+
+def matmul_distributed(x, y, accumulate_into=None, group=None):
+    """``matmul`` (reference matrix.py:349-400) row-sharded over the ranks of
+    ``group`` (one process per GPU): same arguments and result on every
+    rank, byte-identical to the single-GPU product; the saturation flag is
+    set on every rank when any rank saturated."""
+    from .matrix import (DimensionMismatch, TropicalMatrix, _check_same_kind, _check_same_storage, _max_bound,
+                         _rowmajor, _sum_bound)
+    from .semiring import _note_saturation
+
+    _check_same_kind(x, y)
+    if x.n_cols != y.n_rows:
+        raise DimensionMismatch(f"matmul inner dimensions differ: {x.shape} x {y.shape}")
+    _check_same_storage(x, y)
+    integer = x.integer and y.integer
+    z = None
+    if accumulate_into is not None:
+        _check_same_kind(x, accumulate_into)
+        if accumulate_into.shape != (x.n_rows, y.n_cols):
+            raise DimensionMismatch(
+                f"accumulate_into shape {accumulate_into.shape} does not match output {(x.n_rows, y.n_cols)}")
+        _check_same_storage(x, accumulate_into)
+        integer = integer and accumulate_into.integer
+        z = _rowmajor(accumulate_into.data)
+    out, sat = matmul_sharded(_rowmajor(x.data), _rowmajor(y.data), x.kind, integer, z=z, group=group)
+    if sat:
+        _note_saturation()
+    bound = _sum_bound(x.abs_bound, y.abs_bound)
+    if accumulate_into is not None:
+        bound = _max_bound(bound, accumulate_into.abs_bound)
+    return TropicalMatrix._wrap(x.kind, out, integer, bound)
+
+
+def matvec_distributed(a, v, group=None):
+    """``matvec`` (reference matrix.py:403-425) with the rows of ``a`` split
+    over the ranks: each rank streams only its rows of A from HBM (the
+    HBM-bound pass scales with P) and the n-element result is all-gathered.
+    Same result on every rank, byte-identical to matvec."""
+    from .matrix import (DimensionMismatch, TropicalVector, _check_same_kind, _check_same_storage, _matvec,
+                         _rowmajor, _sum_bound)
+    from .semiring import _note_saturation
+
+    _check_same_kind(a, v)
+    if a.n_cols != len(v):
+        raise DimensionMismatch(f"matvec dimensions differ: {a.shape} x {len(v)}")
+    _check_same_storage(a, v)
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    m = a.n_rows
+    dev = a.device
+    chunk, spans = partition(m, world, 1)
+    r0, r1 = spans[rank]
+    integer = a.integer and v.integer
+    full = torch.empty((world * chunk,), dtype=a.dtype, device=dev)
+    sat = torch.zeros(1, dtype=torch.int32, device=dev)
+    if r1 > r0:
+        out, flags = _matvec(_rowmajor(a.data)[r0:r1], v.data.reshape(1, -1), a.kind, integer,
+                             _sum_bound(a.abs_bound, v.abs_bound))
+        full[r0:r1].copy_(out.reshape(-1))
+        sat = flags[_lib.FLAG_SATURATED].reshape(1).clone()
+    dist.all_gather_into_tensor(full, full[rank * chunk : (rank + 1) * chunk], group=group)
+    dist.all_reduce(sat, op=dist.ReduceOp.MAX, group=group)
+    if int(_host_read(sat)[0]):
+        _note_saturation()
+    return TropicalVector._wrap(a.kind, full[:m].clone(), integer, _sum_bound(a.abs_bound, v.abs_bound))
 
 
 # ---------------------------------------------------------------------------
