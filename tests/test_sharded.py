@@ -81,3 +81,60 @@ def test_sharded_squaring_gloo_world2():
             assert gneg == neg and gm == mults, (idx, rank)
             if not neg:
                 assert got == want.tobytes(), (idx, rank)
+
+
+def _oracle_gemm_plain(a_rows, b, out, z_rows=None, peers=None):
+    c, sat = ot.matmul(a_rows.numpy(), b.numpy(), ot.MIN, "f64", True, acc=None if z_rows is None else z_rows.numpy())
+    out.copy_(torch.from_numpy(c))
+    return torch.tensor([int(sat)], dtype=torch.int32)
+
+
+def _matmul_cases():
+    rng = np.random.default_rng(21)
+    out = []
+    for m, k, n in ((1, 1, 1), (5, 7, 3), (130, 40, 17), (9, 300, 250)):
+        x = rng.integers(-50, 100, (m, k)).astype(float)
+        y = rng.integers(-50, 100, (k, n)).astype(float)
+        z = rng.integers(-50, 100, (m, n)).astype(float)
+        for a in (x, y, z):
+            a[rng.random(a.shape) < 0.25] = math.inf
+        out.append((x, y, z))
+    big = 2.0**53 - 1  # one saturating product on one rank only
+    out.append((np.array([[big], [1.0]]), np.array([[big]]), np.zeros((2, 1))))
+    return out
+
+
+def _matmul_worker(rank, world, port, results):
+    from paper_1701_04733_b200.sharded import matmul_sharded
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        for idx, (x, y, z) in enumerate(_matmul_cases()):
+            for acc in (False, True):
+                xt, yt = torch.from_numpy(ot.orient(ot.MIN, x)), torch.from_numpy(ot.orient(ot.MIN, y))
+                zt = torch.from_numpy(ot.orient(ot.MIN, z)) if acc else None
+                out, sat = matmul_sharded(xt, yt, None, True, z=zt, gemm_rows=_oracle_gemm_plain, align=1)
+                results[(rank, idx, acc)] = (out.numpy().tobytes(), sat)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_sharded_matmul_gloo_world2():
+    """matmul_sharded (row blocks + all-gather + saturation all-reduce) on two
+    gloo ranks: every rank holds the full product, byte-identical to the
+    single-process restatement of btas.matmul, saturation seen everywhere."""
+    world = 2
+    port = _free_port()
+    manager = mp.get_context("spawn").Manager()
+    results = manager.dict()
+    mp.spawn(_matmul_worker, args=(world, port, results), nprocs=world, join=True)
+    for idx, (x, y, z) in enumerate(_matmul_cases()):
+        for acc in (False, True):
+            want, sat = ot.matmul(ot.orient(ot.MIN, x), ot.orient(ot.MIN, y), ot.MIN, "f64", True,
+                                  acc=ot.orient(ot.MIN, z) if acc else None)
+            for rank in range(world):
+                got, gsat = results[(rank, idx, acc)]
+                assert got == want.tobytes() and gsat == sat, (idx, acc, rank)
