@@ -230,41 +230,51 @@ int btas_fw(int dtype, int integer_mode, void* D, int64_t ld, int64_t n, int mas
             double max_abs, double min_finite, int32_t* dev_flags,
             void* workspace, size_t workspace_bytes, btas_stream_t stream);
 
-/* Row-sharded Floyd-Warshall for P processes (one per GPU): the same
- * per-round operands as btas_fw, one pivot block kb at a time.  Each rank
- * holds rows [slab_r0, slab_r0 + slab_rows) of D (slab_r0 a multiple of 128)
- * at D_slab.  Per pivot block the host runs, in order:
- *   PIVOT   on the rank owning row block kb (phase 1 + row panel),
+/* Row-sharded Floyd-Warshall for P processes (one per GPU) with lookahead
+ * groups: the same per-round operands as btas_fw.  Each rank holds rows
+ * [slab_r0, slab_r0 + slab_rows) of D (slab_r0 a multiple of 128) at D_slab.
+ * Pivot blocks (b = 128 rows, 64 for float64) are processed in groups of
+ * up to btas_fw_dist_group_size(dtype) consecutive blocks [kb0, kb0 +
+ * group_blocks) that lie inside ONE rank's slab (its owner).  Per group the
+ * host runs, in order:
+ *   OWNER   on the owner: for each block of the group, the pending updates of
+ *           the group's earlier blocks into its row / column panels, phase 1,
+ *           the row panel and the column panel over the owner's rows,
  *   a broadcast of the owner's workspace bytes [bcast_offset, +bcast_bytes)
- *           to every rank (NCCL over NVLink),
- *   COLS    on every rank (column panels of its rows),
- *   UPDATE  on every rank (phase-3 update of its rows);
- * INIT once before the first block and DIAG once at the end.  `masked` and
- * `min_finite` must be the same on every rank (all-reduced scan of D). */
+ *           to every rank (one NCCL broadcast per group; or fused: see
+ *           btas_fw_dist_group_peers),
+ *   REST    on every rank: a non-owner's column panels for each block of the
+ *           group, then the update of the rank's rows by the whole group in
+ *           one GEMM pass (K = group_blocks * b);
+ * INIT once before the first group and DIAG once at the end.  `masked` and
+ * `min_finite` must be the same on every rank (all-reduced scan of D).  One
+ * exchange per group instead of per pivot block (replaces the reference
+ * rounds of apsp.py:108-123, byte-identical for any P). */
 enum {
   BTAS_FW_STAGE_INIT = 0,
-  BTAS_FW_STAGE_PIVOT = 1,
-  BTAS_FW_STAGE_COLS = 2,
-  BTAS_FW_STAGE_UPDATE = 3,
-  BTAS_FW_STAGE_DIAG = 4
+  BTAS_FW_STAGE_DIAG = 4,
+  BTAS_FW_STAGE_OWNER = 5,
+  BTAS_FW_STAGE_REST = 6
 };
+int btas_fw_dist_group_size(int dtype);
 size_t btas_fw_dist_workspace_bytes(int dtype, int64_t n, int64_t slab_rows, size_t* bcast_offset,
                                     size_t* bcast_bytes);
-int btas_fw_dist_stage(int dtype, int integer_mode, int stage, void* D_slab, int64_t ld, int64_t n,
-                       int64_t slab_r0, int64_t slab_rows, int64_t kb, int masked, double min_finite,
-                       int32_t* dev_flags, void* workspace, size_t workspace_bytes, btas_stream_t stream);
-/* btas_fw_dist_stage with the pivot-panel broadcast fused into the PIVOT
- * stage: every store the owner's phase-1 / row-panel kernels make into its
- * broadcast region is repeated, at the same offset, in peer_regions[0..n_peers)
- * (n_peers <= 7): the other ranks' broadcast regions (their workspace +
- * bcast_offset) mapped into this process (NVLink peer memory / CUDA IPC).
- * The caller replaces the broadcast by a barrier that orders the peers'
- * COLS stage after this PIVOT stage, and alternates two workspaces by the
- * parity of kb so the next owner's stores never overwrite a region a peer is
- * still reading.  Other stages ignore the peers. */
-int btas_fw_dist_stage_peers(int dtype, int integer_mode, int stage, void* D_slab, int64_t ld, int64_t n,
-                             int64_t slab_r0, int64_t slab_rows, int64_t kb, int masked, double min_finite,
-                             int32_t* dev_flags, void* workspace, size_t workspace_bytes,
+int btas_fw_dist_group(int dtype, int integer_mode, int stage, void* D_slab, int64_t ld, int64_t n,
+                       int64_t slab_r0, int64_t slab_rows, int64_t kb0, int group_blocks, int masked,
+                       double min_finite, int32_t* dev_flags, void* workspace, size_t workspace_bytes,
+                       btas_stream_t stream);
+/* btas_fw_dist_group with the broadcast fused into the OWNER stage: every
+ * store the owner's kernels make into its broadcast region is repeated, at
+ * the same offset, in peer_regions[0..n_peers) (n_peers <= 7): the other
+ * ranks' broadcast regions (their workspace + bcast_offset) mapped into this
+ * process (NVLink peer memory / CUDA IPC).  The caller replaces the
+ * broadcast by a barrier that orders the peers' REST stage after this OWNER
+ * stage, and alternates two workspaces by the parity of the group so the
+ * next owner's stores never overwrite a region a peer is still reading.
+ * Other stages ignore the peers. */
+int btas_fw_dist_group_peers(int dtype, int integer_mode, int stage, void* D_slab, int64_t ld, int64_t n,
+                             int64_t slab_r0, int64_t slab_rows, int64_t kb0, int group_blocks, int masked,
+                             double min_finite, int32_t* dev_flags, void* workspace, size_t workspace_bytes,
                              void* const* peer_regions, int n_peers, btas_stream_t stream);
 
 /* Diagonal test: sets BTAS_FLAG_DIAG_NEG if any d[i,i] < 0 (apsp.py:125,168). */

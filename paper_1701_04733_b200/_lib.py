@@ -122,9 +122,11 @@ SIGNATURES = {
     "btas_fw_workspace_bytes": (_sz, [_i32, _i64]),
     "btas_fw": (_i32, [_i32, _i32, _p, _i64, _i64, _i32, _dbl, _dbl, _p, _p, _sz, _p]),
     "btas_fw_dist_workspace_bytes": (_sz, [_i32, _i64, _i64, ctypes.POINTER(_sz), ctypes.POINTER(_sz)]),
-    "btas_fw_dist_stage": (_i32, [_i32, _i32, _i32, _p, _i64, _i64, _i64, _i64, _i64, _i32, _dbl, _p, _p, _sz, _p]),
-    "btas_fw_dist_stage_peers": (_i32, [_i32, _i32, _i32, _p, _i64, _i64, _i64, _i64, _i64, _i32, _dbl, _p, _p, _sz,
-                                        ctypes.POINTER(_p), _i32, _p]),
+    "btas_fw_dist_group_size": (_i32, [_i32]),
+    "btas_fw_dist_group": (_i32, [_i32, _i32, _i32, _p, _i64, _i64, _i64, _i64, _i64, _i32, _i32, _dbl, _p, _p, _sz,
+                                  _p]),
+    "btas_fw_dist_group_peers": (_i32, [_i32, _i32, _i32, _p, _i64, _i64, _i64, _i64, _i64, _i32, _i32, _dbl, _p, _p,
+                                        _sz, ctypes.POINTER(_p), _i32, _p]),
     "btas_diag_negative": (_i32, [_i32, _p, _i64, _i64, _p, _p]),
     "btas_probe_ceiling": (_i32, [_i32, ctypes.POINTER(_dbl), ctypes.POINTER(_dbl), ctypes.POINTER(_dbl)]),
     "btas_apsp_small_workspace_bytes": (_sz, [_i32, _i64]),

@@ -695,15 +695,29 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
 }
 
 // ------------------------------------------------------------------ distributed
-// Row-slab Floyd-Warshall for P processes (one per GPU), one pivot block at a
-// time (no lookahead): the owner of pivot block kb runs phase 1 and the row
-// panel, the "broadcast region" of its workspace (pivot snapshots, packed
-// row-panel snapshots in both forms, the s16 flag) is broadcast by the host
-// (NCCL), then every rank runs the column panels and the phase-3 update of its
-// own rows.  Same per-round candidates as the single-GPU program, so D is
-// byte-identical for any P.
+// Row-slab Floyd-Warshall for P processes (one per GPU) with the single-GPU
+// lookahead.  Pivot blocks are taken in GROUPS of up to G::look consecutive
+// blocks that lie inside one rank's slab (the owner).  Per group:
+//   OWNER (owner only): for each block j of the group, the pending updates
+//     of the group's earlier blocks go into the block's row panel and into
+//     its column panel over the owner's rows (thin passes, K = j*b), then
+//     phase 1, the row panel (phase 2, emits Srow slot j) and the column
+//     panel over the owner's rows (emits Scol slot j);
+//   exchange: the owner's "broadcast region" — the s16 flag, the pivot-row
+//     snapshots of every block of the group and the packed Srow slots in both
+//     forms — reaches every rank: stored into the peers' regions by the
+//     owner's kernels as they produce it (fused, btas_fw_dist_group_peers)
+//     or one NCCL broadcast per group; the host orders REST after it;
+//   REST (every rank): a non-owner runs, for each block j, the thin pass of
+//     the earlier blocks into its column panel rows and the column panel
+//     itself (emits its Scol slot j); then every rank applies all the
+//     group's blocks to its rows in ONE GEMM pass with K = m*b.
+// The candidates are those of the single-GPU program (same per-round
+// snapshots; re-applying a block's candidates is a no-op under min), so D is
+// byte-identical for any P, and the bulk pass does m times the add-min work
+// per epilogue with one exchange per group instead of per block.
 struct FwDistWs {
-  size_t ctrl, rsp, csp, srow, srow16, bcast_end, scol, scol16, total;
+  size_t ctrl, rsp, srow, srow16, bcast_end, csp, scol, scol16, total;
 };
 
 template <class T>
@@ -715,29 +729,29 @@ FwDistWs fw_dist_ws(int64_t n, int64_t slab_rows) {
   size_t off = 0;
   w.ctrl = off;
   off += a256(sizeof(FwCtrl));
-  w.rsp = off;
-  off += a256((size_t)G::b * G::b * sizeof(T));
-  w.csp = off;
-  off += a256((size_t)G::b * G::b * sizeof(T));
+  w.rsp = off;  // pivot-row snapshots of every block of the group
+  off += a256((size_t)G::look * G::b * G::b * sizeof(T));
   w.srow = off;
-  off += a256((size_t)cols * G::b * sizeof(T));
+  off += a256((size_t)cols * G::look * G::b * sizeof(T));
   w.srow16 = off;
-  off += a256((size_t)cols * (G::b / 2) * 4);
+  off += a256((size_t)cols * G::look * (G::b / 2) * 4);
   w.bcast_end = off;
+  w.csp = off;  // pivot-column snapshot (owner-local)
+  off += a256((size_t)G::b * G::b * sizeof(T));
   w.scol = off;
-  off += a256((size_t)rows * G::b * sizeof(T));
+  off += a256((size_t)rows * G::look * G::b * sizeof(T));
   w.scol16 = off;
-  off += a256((size_t)rows * (G::b / 2) * 4);
+  off += a256((size_t)rows * G::look * (G::b / 2) * 4);
   w.total = off;
   return w;
 }
 
 template <class T, int MODE>
-int fw_dist_stage_typed(int integer_mode, int stage, T* D, int64_t ld, int64_t n, int64_t slab_r0, int64_t slab_rows,
-                        int64_t kb, int32_t* flags, unsigned char* ws, void* const* peers, int n_peers,
-                        cudaStream_t st) {
+int fw_dist_group_typed(int integer_mode, int stage, T* D, int64_t ld, int64_t n, int64_t slab_r0,
+                        int64_t slab_rows, int64_t kb0, int m, int32_t* flags, unsigned char* ws, void* const* peers,
+                        int n_peers, cudaStream_t st) {
   using G = FwGeom<T>;
-  constexpr int b = G::b;
+  constexpr int b = G::b, kLook = G::look;
   constexpr bool CHECKED = MODE == kChecked;
   const FwDistWs W = fw_dist_ws<T>(n, slab_rows);
   const int nblk = (int)ceil_div(n, b);
@@ -751,23 +765,28 @@ int fw_dist_stage_typed(int integer_mode, int stage, T* D, int64_t ld, int64_t n
   uint32_t* srow16 = reinterpret_cast<uint32_t*>(ws + W.srow16);
   T* scol = reinterpret_cast<T*>(ws + W.scol);
   uint32_t* scol16 = reinterpret_cast<uint32_t*>(ws + W.scol16);
-  const int64_t rows_pad = (int64_t)((W.scol16 - W.scol) / sizeof(T)) / b;
+  const int64_t rows_pad = (int64_t)((W.scol16 - W.scol) / sizeof(T)) / ((int64_t)kLook * b);
+  const int64_t cols = fw_cols<T>(n);
+  const int64_t k_lo = kb0 * b, k_hi = std::min<int64_t>(n, (kb0 + m) * b);
+  const bool owner = slab_rows > 0 && k_lo >= slab_r0 && k_lo < slab_r0 + slab_rows;
+  if (stage != BTAS_FW_STAGE_INIT && stage != BTAS_FW_STAGE_DIAG) {
+    if (m < 1 || m > kLook || kb0 < 0 || k_lo >= n) return BTAS_ERR_INVALID;
+    if (owner && k_hi > slab_r0 + slab_rows) return BTAS_ERR_INVALID;  // a group never spans two slabs
+    if (stage == BTAS_FW_STAGE_OWNER && !owner) return BTAS_ERR_INVALID;
+  }
 
   FwArgs f{};
   f.n = n;
   f.ld = ld;
   f.slab_r0 = slab_r0;
   f.slab_r1 = slab_r0 + slab_rows;
-  f.k0 = kb * b;
   f.nblk = nblk;
   f.int_mode = int_mode ? 1 : 0;
   f.limit = limit;
   f.BMa = G::BMa;
   f.BNb = G::BNb;
-  f.Kp2 = b / 2;
-  f.Kp2w = b / 4;
-  f.koff = 0;
-  f.group_start = 1;
+  f.Kp2 = (int64_t)kLook * b / 2;  // panels hold kLook pivot blocks of k
+  f.Kp2w = (int64_t)kLook * b / 4;
   f.emit_s16 = emit_s16 ? 1 : 0;
   f.flags = flags;
   f.ctrl = ctrl;
@@ -788,6 +807,88 @@ int fw_dist_stage_typed(int integer_mode, int stage, T* D, int64_t ld, int64_t n
     }
     mark_configured(configured);
   }
+
+  // GEMM descriptors over this rank's slab (rows slab-local); per launch only
+  // the k range (slots), the row/column window and the skips change
+  GemmArgs g{};
+  g.Ap = scol;
+  g.Bp = srow;
+  g.Kp2 = b / 2;
+  g.Kp2s = (int64_t)kLook * b / 2;
+  g.M = slab_rows;
+  g.N = n;
+  g.mblocks = (int)(rows_pad / G::BMa);
+  g.nblocks = (int)(cols / G::BNb);
+  g.Z = D;
+  g.ldz = ld;
+  g.C = D;
+  g.ldc = ld;
+  g.flags = flags;
+  g.integer_mode = int_mode ? 1 : 0;
+  g.limit = int_mode ? limit : INFINITY;
+  g.gate = emit_s16 ? &ctrl->s16_overflow[0] : nullptr;
+  g.gate_value = 1;
+  g.no_diag = 1;
+  g.skip_row_lo = g.skip_row_hi = g.skip_col_lo = g.skip_col_hi = 0;
+  GemmArgs g16 = g;
+  g16.Ap = scol16;
+  g16.Bp = srow16;
+  g16.Kp2 = b / 4;
+  g16.Kp2s = (int64_t)kLook * b / 4;
+  g16.mblocks = (int)(round_up(rows_pad, 128) / 128);
+  g16.nblocks = (int)(round_up(cols, 128) / 128);
+  g16.gate = &ctrl->s16_overflow[0];
+  g16.gate_value = 0;
+  g16.limit = limit;
+  g16.integer_mode = 1;
+  // one update over K = slots * b (group slots [0, slots)): 32-bit kernel
+  // gated on "s16 overflow", s16x2 kernel gated on "no overflow"
+  auto update = [&](GemmArgs a, GemmArgs a16, int slots) -> int {
+    a.Kp2 = (int64_t)slots * b / 2;
+    a16.Kp2 = (int64_t)slots * b / 4;
+    int rc;
+    if constexpr (CHECKED) rc = launch_gemm_epi<MixChecked<T, true>, true, kEpiAcc>(a, st);
+    else if constexpr (Traits<T>::dtype == BTAS_F64) rc = launch_gemm_epi<MixF64<true>, true, kEpiAcc>(a, st);
+    else if constexpr (Traits<T>::dtype == BTAS_I32) rc = launch_gemm_epi<MixI32<true>, true, kEpiAcc>(a, st);
+    else rc = launch_gemm_epi<MixF32<true>, true, kEpiAcc>(a, st);
+    if (rc) return rc;
+    if (emit_s16) rc = launch_gemm_epi<MixS16<true, T>, true, kEpiAcc>(a16, st);
+    return rc;
+  };
+  // pending updates (slots 0..j-1) -> column block kb over this rank's rows
+  // (the owner skips the block's own rows: the row pass covers them)
+  auto thin_cols = [&](int64_t kb, int j) -> int {
+    const int64_t kk = kb * b;
+    GemmArgs a = g, a16 = g16;
+    a.N = a16.N = std::min<int64_t>(b, n - kk);
+    a.nblocks = a16.nblocks = 1;
+    a.Bp = srow + (size_t)kb * g.Kp2s * G::BNb * 2;
+    a16.Bp = srow16 + (size_t)kb * g16.Kp2s * 128 * 2;
+    a.C = a16.C = D + kk;
+    a.Z = a16.Z = D + kk;
+    if (owner) {
+      a.skip_row_lo = a16.skip_row_lo = kk - slab_r0;
+      a.skip_row_hi = a16.skip_row_hi = kk - slab_r0 + b;
+    }
+    return update(a, a16, j);
+  };
+  // phase 2 column panel over this rank's row blocks for block kb (slot j)
+  auto cols_panel = [&](int64_t kb, int j) -> int {
+    if (nblk == 1) return BTAS_OK;
+    FwArgs fc = f;
+    fc.k0 = kb * b;
+    fc.koff = j * b;
+    fc.group_start = 0;
+    fc.panel_mode = 2;
+    fc.col_blk0 = (int)(slab_r0 / b);
+    fc.n_peers = 0;  // column panels are rank-local
+    const int nsb = (int)ceil_div(slab_rows, b);
+    fw_phase2_kernel<T, MODE><<<dim3(nsb, 1), kFw2Threads, smem2, st>>>(D, rsp + (size_t)j * b * b, csp, scol, srow,
+                                                                       scol16, srow16, fc);
+    BTAS_CUDA_CHECK_LAUNCH();
+    return BTAS_OK;
+  };
+  int rc;
   switch (stage) {
     case BTAS_FW_STAGE_INIT: {
       // packed panels: padding rows/cols hold Infinity
@@ -798,68 +899,58 @@ int fw_dist_stage_typed(int integer_mode, int stage, T* D, int64_t ld, int64_t n
       fill_u32_kernel<<<1024, 256, 0, st>>>(scol16, (int64_t)((W.total - W.scol16) / 4), inf16);
       break;
     }
-    case BTAS_FW_STAGE_PIVOT: {
-      if (f.k0 < slab_r0 || f.k0 >= slab_r0 + slab_rows) return BTAS_ERR_INVALID;  // not the owner
-      fw_phase1_kernel<T, MODE><<<1, kFw1Threads, smem, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
-      if (nblk > 1) {
-        f.panel_mode = 1;
-        fw_phase2_kernel<T, MODE><<<dim3(nblk, 1), kFw2Threads, smem2, st>>>(D, rsp, csp, scol, srow, scol16, srow16,
-                                                                            f);
+    case BTAS_FW_STAGE_OWNER: {
+      for (int j = 0; j < m; ++j) {
+        const int64_t kb = kb0 + j, kk = kb * b;
+        if (j > 0) {
+          {  // pending updates -> row panel kb (pivot rows x every column)
+            GemmArgs a = g, a16 = g16;
+            a.M = a16.M = std::min<int64_t>(b, n - kk);
+            a.mblocks = a16.mblocks = 1;
+            a.Ap = scol + (size_t)((kk - slab_r0) / G::BMa) * g.Kp2s * G::BMa * 2;
+            a16.Ap = scol16 + (size_t)((kk - slab_r0) / 128) * g16.Kp2s * 128 * 2;
+            a.C = a16.C = D + (kk - slab_r0) * ld;
+            a.Z = a16.Z = D + (kk - slab_r0) * ld;
+            if ((rc = update(a, a16, j))) return rc;
+          }
+          if ((rc = thin_cols(kb, j))) return rc;
+        }
+        FwArgs fp = f;
+        fp.k0 = kk;
+        fp.koff = j * b;
+        fp.group_start = j == 0;
+        T* rsp_j = rsp + (size_t)j * b * b;
+        fw_phase1_kernel<T, MODE><<<1, kFw1Threads, smem, st>>>(D, rsp_j, csp, scol, srow, scol16, srow16, fp);
+        if (nblk > 1) {
+          fp.panel_mode = 1;
+          fw_phase2_kernel<T, MODE><<<dim3(nblk, 1), kFw2Threads, smem2, st>>>(D, rsp_j, csp, scol, srow, scol16,
+                                                                              srow16, fp);
+        }
+        BTAS_CUDA_CHECK_LAUNCH();
+        if ((rc = cols_panel(kb, j))) return rc;
       }
       break;
     }
-    case BTAS_FW_STAGE_COLS: {
-      if (slab_rows == 0 || nblk == 1) break;
-      f.panel_mode = 2;
-      f.col_blk0 = (int)(slab_r0 / b);
-      const int nsb = (int)ceil_div(slab_rows, b);
-      fw_phase2_kernel<T, MODE><<<dim3(nsb, 1), kFw2Threads, smem2, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
-      break;
-    }
-    case BTAS_FW_STAGE_UPDATE: {
-      if (slab_rows == 0 || nblk == 1) break;
-      GemmArgs g{};
-      g.Ap = scol;
-      g.Bp = srow;
-      g.Kp2 = b / 2;
-      g.M = slab_rows;
-      g.N = n;
-      g.mblocks = (int)(rows_pad / G::BMa);
-      g.nblocks = (int)(fw_cols<T>(n) / G::BNb);
-      g.Z = D;
-      g.ldz = ld;
-      g.C = D;
-      g.ldc = ld;
-      g.flags = flags;
-      g.integer_mode = int_mode ? 1 : 0;
-      g.limit = int_mode ? limit : INFINITY;
-      g.no_diag = 1;
-      g.skip_row_lo = f.k0 - slab_r0;
-      g.skip_row_hi = f.k0 - slab_r0 + b;
-      g.skip_col_lo = f.k0;
-      g.skip_col_hi = f.k0 + b;
-      g.gate = emit_s16 ? &ctrl->s16_overflow[0] : nullptr;
-      g.gate_value = 1;
-      GemmArgs g16 = g;
-      g16.Ap = scol16;
-      g16.Bp = srow16;
-      g16.Kp2 = b / 4;
-      g16.mblocks = (int)(round_up(rows_pad, 128) / 128);
-      g16.nblocks = (int)(round_up(fw_cols<T>(n), 128) / 128);
-      g16.gate = &ctrl->s16_overflow[0];
-      g16.gate_value = 0;
-      g16.limit = limit;
-      g16.integer_mode = 1;
-      int rc;
-      if constexpr (CHECKED) rc = launch_gemm_epi<MixChecked<T, true>, true, kEpiAcc>(g, st);
-      else if constexpr (Traits<T>::dtype == BTAS_F64) rc = launch_gemm_epi<MixF64<true>, true, kEpiAcc>(g, st);
-      else if constexpr (Traits<T>::dtype == BTAS_I32) rc = launch_gemm_epi<MixI32<true>, true, kEpiAcc>(g, st);
-      else rc = launch_gemm_epi<MixF32<true>, true, kEpiAcc>(g, st);
-      if (rc) return rc;
-      if (emit_s16) {
-        rc = launch_gemm_epi<MixS16<true, T>, true, kEpiAcc>(g16, st);
-        if (rc) return rc;
+    case BTAS_FW_STAGE_REST: {
+      if (slab_rows == 0) break;
+      if (!owner) {
+        for (int j = 0; j < m; ++j) {
+          if (j > 0 && (rc = thin_cols(kb0 + j, j))) return rc;
+          if ((rc = cols_panel(kb0 + j, j))) return rc;
+        }
       }
+      if (nblk == 1) break;
+      // every group block on every tile of this rank outside the last
+      // block's row/column panels, K = m*b in one pass
+      const int64_t kl = (kb0 + m - 1) * b;
+      GemmArgs a = g, a16 = g16;
+      a.skip_col_lo = a16.skip_col_lo = kl;
+      a.skip_col_hi = a16.skip_col_hi = kl + b;
+      if (owner) {
+        a.skip_row_lo = a16.skip_row_lo = kl - slab_r0;
+        a.skip_row_hi = a16.skip_row_hi = kl - slab_r0 + b;
+      }
+      if ((rc = update(a, a16, m))) return rc;
       break;
     }
     case BTAS_FW_STAGE_DIAG:
@@ -950,10 +1041,23 @@ extern "C" size_t btas_fw_dist_workspace_bytes(int dtype, int64_t n, int64_t sla
   return total;
 }
 
-static int fw_dist_stage_entry(int dtype, int integer_mode, int stage, void* D_slab, int64_t ld, int64_t n,
-                               int64_t slab_r0, int64_t slab_rows, int64_t kb, int masked, double min_finite,
-                               int32_t* dev_flags, void* workspace, size_t workspace_bytes, void* const* peers,
-                               int n_peers, btas_stream_t stream) {
+extern "C" int btas_fw_dist_group_size(int dtype) {
+  switch (dtype) {
+    case BTAS_F32:
+      return FwGeom<float>::look;
+    case BTAS_I32:
+      return FwGeom<int32_t>::look;
+    case BTAS_F64:
+      return FwGeom<double>::look;
+    default:
+      return 0;
+  }
+}
+
+static int fw_dist_group_entry(int dtype, int integer_mode, int stage, void* D_slab, int64_t ld, int64_t n,
+                               int64_t slab_r0, int64_t slab_rows, int64_t kb0, int group_blocks, int masked,
+                               double min_finite, int32_t* dev_flags, void* workspace, size_t workspace_bytes,
+                               void* const* peers, int n_peers, btas_stream_t stream) {
   if (!dev_flags || !workspace || n < 1 || ld < n || slab_r0 < 0 || slab_rows < 0 || slab_r0 + slab_rows > n)
     return BTAS_ERR_INVALID;
   if (n_peers < 0 || n_peers > 7 || (n_peers > 0 && !peers)) return BTAS_ERR_INVALID;
@@ -961,18 +1065,18 @@ static int fw_dist_stage_entry(int dtype, int integer_mode, int stage, void* D_s
     if (!peers[q]) return BTAS_ERR_INVALID;
   if (slab_rows > 0 && !D_slab) return BTAS_ERR_INVALID;
   const int64_t b = dtype == BTAS_F64 ? 64 : 128;
-  if ((slab_rows > 0 && slab_r0 % 128 != 0) || kb < 0 || kb * b >= n) return BTAS_ERR_INVALID;
+  if ((slab_rows > 0 && slab_r0 % 128 != 0) || kb0 < 0 || kb0 * b >= n) return BTAS_ERR_INVALID;
   if (workspace_bytes < btas_fw_dist_workspace_bytes(dtype, n, slab_rows, nullptr, nullptr)) return BTAS_ERR_WORKSPACE;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   unsigned char* ws = static_cast<unsigned char*>(workspace);
-#define BTAS_FWD_CALL(T)                                                                                          \
-  (masked ? fw_dist_stage_typed<T, kChecked>(integer_mode, stage, (T*)D_slab, ld, n, slab_r0, slab_rows, kb,      \
-                                             dev_flags, ws, peers, n_peers, st)                                   \
-   : (dtype == BTAS_I32 && min_finite < 0.0)                                                                      \
-       ? fw_dist_stage_typed<T, kClamp>(integer_mode, stage, (T*)D_slab, ld, n, slab_r0, slab_rows, kb, dev_flags, \
-                                        ws, peers, n_peers, st)                                                   \
-       : fw_dist_stage_typed<T, kFast>(integer_mode, stage, (T*)D_slab, ld, n, slab_r0, slab_rows, kb, dev_flags,  \
-                                       ws, peers, n_peers, st))
+#define BTAS_FWD_CALL(T)                                                                                           \
+  (masked ? fw_dist_group_typed<T, kChecked>(integer_mode, stage, (T*)D_slab, ld, n, slab_r0, slab_rows, kb0,      \
+                                             group_blocks, dev_flags, ws, peers, n_peers, st)                      \
+   : (dtype == BTAS_I32 && min_finite < 0.0)                                                                       \
+       ? fw_dist_group_typed<T, kClamp>(integer_mode, stage, (T*)D_slab, ld, n, slab_r0, slab_rows, kb0,           \
+                                        group_blocks, dev_flags, ws, peers, n_peers, st)                           \
+       : fw_dist_group_typed<T, kFast>(integer_mode, stage, (T*)D_slab, ld, n, slab_r0, slab_rows, kb0,            \
+                                       group_blocks, dev_flags, ws, peers, n_peers, st))
   switch (dtype) {
     case BTAS_F32:
       return BTAS_FWD_CALL(float);
@@ -986,18 +1090,19 @@ static int fw_dist_stage_entry(int dtype, int integer_mode, int stage, void* D_s
 #undef BTAS_FWD_CALL
 }
 
-extern "C" int btas_fw_dist_stage(int dtype, int integer_mode, int stage, void* D_slab, int64_t ld, int64_t n,
-                                  int64_t slab_r0, int64_t slab_rows, int64_t kb, int masked, double min_finite,
-                                  int32_t* dev_flags, void* workspace, size_t workspace_bytes, btas_stream_t stream) {
-  return fw_dist_stage_entry(dtype, integer_mode, stage, D_slab, ld, n, slab_r0, slab_rows, kb, masked, min_finite,
-                             dev_flags, workspace, workspace_bytes, nullptr, 0, stream);
+extern "C" int btas_fw_dist_group(int dtype, int integer_mode, int stage, void* D_slab, int64_t ld, int64_t n,
+                                  int64_t slab_r0, int64_t slab_rows, int64_t kb0, int group_blocks, int masked,
+                                  double min_finite, int32_t* dev_flags, void* workspace, size_t workspace_bytes,
+                                  btas_stream_t stream) {
+  return fw_dist_group_entry(dtype, integer_mode, stage, D_slab, ld, n, slab_r0, slab_rows, kb0, group_blocks, masked,
+                             min_finite, dev_flags, workspace, workspace_bytes, nullptr, 0, stream);
 }
 
-extern "C" int btas_fw_dist_stage_peers(int dtype, int integer_mode, int stage, void* D_slab, int64_t ld, int64_t n,
-                                        int64_t slab_r0, int64_t slab_rows, int64_t kb, int masked,
-                                        double min_finite, int32_t* dev_flags, void* workspace,
+extern "C" int btas_fw_dist_group_peers(int dtype, int integer_mode, int stage, void* D_slab, int64_t ld, int64_t n,
+                                        int64_t slab_r0, int64_t slab_rows, int64_t kb0, int group_blocks,
+                                        int masked, double min_finite, int32_t* dev_flags, void* workspace,
                                         size_t workspace_bytes, void* const* peer_regions, int n_peers,
                                         btas_stream_t stream) {
-  return fw_dist_stage_entry(dtype, integer_mode, stage, D_slab, ld, n, slab_r0, slab_rows, kb, masked, min_finite,
-                             dev_flags, workspace, workspace_bytes, peer_regions, n_peers, stream);
+  return fw_dist_group_entry(dtype, integer_mode, stage, D_slab, ld, n, slab_r0, slab_rows, kb0, group_blocks, masked,
+                             min_finite, dev_flags, workspace, workspace_bytes, peer_regions, n_peers, stream);
 }

@@ -427,14 +427,14 @@ def matvec_distributed(a, v, group=None):
 # ---------------------------------------------------------------------------
 # row-sharded Floyd-Warshall (pivot-panel broadcast)
 # ---------------------------------------------------------------------------
-FW_STAGE_INIT, FW_STAGE_PIVOT, FW_STAGE_COLS, FW_STAGE_UPDATE, FW_STAGE_DIAG = 0, 1, 2, 3, 4
+FW_STAGE_INIT, FW_STAGE_DIAG, FW_STAGE_OWNER, FW_STAGE_REST = 0, 4, 5, 6
 
 
 class _FwRank:
-    """One rank's slab, workspace(s) and flag words for btas_fw_dist_stage.
+    """One rank's slab, workspace(s) and flag words for btas_fw_dist_group.
     With the fused broadcast the rank holds two workspaces, alternated by the
-    parity of the pivot block (``alloc(nbytes)`` may place them in memory the
-    peers can map)."""
+    parity of the lookahead group (``alloc(nbytes)`` may place them in
+    memory the peers can map)."""
 
     def __init__(self, rank, r0, rows, slab, code, n, dev, nbuf=1, alloc=None):
         import ctypes
@@ -447,54 +447,67 @@ class _FwRank:
                     for _ in range(nbuf)]
         self.flags = torch.zeros(_lib.NUM_FLAGS, dtype=torch.int32, device=dev)
 
-    def ws(self, kb: int) -> torch.Tensor:
-        return self.wss[kb % len(self.wss)]
+    def ws(self, gi: int) -> torch.Tensor:
+        return self.wss[gi % len(self.wss)]
 
-    def region(self, kb: int = 0) -> torch.Tensor:
-        return self.ws(kb)[self.region_off : self.region_off + self.region_bytes]
+    def region(self, gi: int = 0) -> torch.Tensor:
+        return self.ws(gi)[self.region_off : self.region_off + self.region_bytes]
+
+
+def fw_groups(n: int, b: int, chunk: int, look: int) -> "list[tuple[int, int, int]]":
+    """Lookahead groups of the row-sharded FW: (first pivot block, blocks,
+    owner rank) — up to ``look`` consecutive pivot blocks of ``b`` rows, never
+    spanning two ranks' slabs of ``chunk`` rows."""
+    nblk = -(-n // b)
+    out, kb = [], 0
+    while kb < nblk:
+        owner = (kb * b) // chunk
+        slab_end = -(-min(n, (owner + 1) * chunk) // b)  # first block past the owner's rows
+        m = max(1, min(look, slab_end - kb, nblk - kb))
+        out.append((kb, m, owner))
+        kb += m
+    return out
 
 
 def _fw_rows_run(ranks, code, integer, n, ld, masked, min_fin, b, chunk, bcast, peers=None):
-    """The stage sequence of btas_fw_dist_stage (include/btas_cuda.h) over
-    the given local ranks; ``bcast(owner, ranks, kb)`` moves the owner's
-    broadcast region to every rank.  With ``peers(kb, rank) -> [addresses]``
-    the owner's PIVOT stage stores its region into the peers' regions itself
-    (btas_fw_dist_stage_peers) and ``bcast`` is only the barrier (also called
-    once with owner -1 after the INIT stages)."""
+    """The group sequence of btas_fw_dist_group (include/btas_cuda.h) over
+    the given local ranks; ``bcast(owner, ranks, gi)`` moves the owner's
+    broadcast region of group ``gi`` to every rank.  With ``peers(gi, rank)
+    -> [addresses]`` the owner's OWNER stage stores its region into the
+    peers' regions itself (btas_fw_dist_group_peers) and ``bcast`` is only
+    the barrier (also called once with owner -1 after the INIT stages)."""
     import ctypes
 
     from .matrix import _ptr, _stream
 
-    def stage(rk, s, kb=0, buf=None):
-        ws = rk.ws(kb if buf is None else buf)
+    look = int(_lib.load().btas_fw_dist_group_size(code))
+
+    def stage(rk, s, kb0=0, m=1, gi=0):
+        ws = rk.ws(gi)
         ptr = _ptr(rk.slab) if rk.rows > 0 else None
-        args = (code, 1 if integer else 0, s, ptr, ld, n, rk.r0, rk.rows, kb, 1 if masked else 0, min_fin,
+        args = (code, 1 if integer else 0, s, ptr, ld, n, rk.r0, rk.rows, kb0, m, 1 if masked else 0, min_fin,
                 _ptr(rk.flags), _ptr(ws), ws.numel())
-        pr = peers(kb, rk.rank) if (peers is not None and s == FW_STAGE_PIVOT) else None
+        pr = peers(gi, rk.rank) if (peers is not None and s == FW_STAGE_OWNER) else None
         if pr:
             arr = (ctypes.c_void_p * len(pr))(*pr)
-            _lib.call("btas_fw_dist_stage_peers", *args, arr, len(pr), _stream(ws.device))
+            _lib.call("btas_fw_dist_group_peers", *args, arr, len(pr), _stream(ws.device))
         else:
-            _lib.call("btas_fw_dist_stage", *args, _stream(ws.device))
+            _lib.call("btas_fw_dist_group", *args, _stream(ws.device))
 
     for rk in ranks:
         for i in range(len(rk.wss)):
-            stage(rk, FW_STAGE_INIT, 0, buf=i)
+            stage(rk, FW_STAGE_INIT, gi=i)
     if peers is not None:
         # the peers' INIT (padding fill of their regions) must finish before
         # any owner stores a panel into them
         bcast(-1, ranks, -1)
-    nblk = -(-n // b)
-    for kb in range(nblk):
-        owner = (kb * b) // chunk
+    for gi, (kb0, m, owner) in enumerate(fw_groups(n, b, chunk, look)):
         for rk in ranks:
             if rk.rank == owner:
-                stage(rk, FW_STAGE_PIVOT, kb)
-        bcast(owner, ranks, kb)
+                stage(rk, FW_STAGE_OWNER, kb0, m, gi)
+        bcast(owner, ranks, gi)
         for rk in ranks:
-            stage(rk, FW_STAGE_COLS, kb)
-        for rk in ranks:
-            stage(rk, FW_STAGE_UPDATE, kb)
+            stage(rk, FW_STAGE_REST, kb0, m, gi)
     for rk in ranks:
         stage(rk, FW_STAGE_DIAG)
 
@@ -536,27 +549,23 @@ def _fw_report(adj, d, negative):
                       negative_cycle=negative, multiplications_performed=0)
 
 
-def _fw_peer_workspaces(nbytes, dev, group, world):
-    """Two symmetric-memory workspaces and, per workspace, the other ranks'
-    base addresses (None when symmetric memory is unavailable)."""
-    got = _peer_buffers((nbytes,), torch.uint8, dev, group, world)
-    return got
-
-
 def floyd_warshall_distributed(adj, group=None, peer_workspaces=None):
     """``floyd_warshall`` (reference apsp.py:93-133) with D row-sharded over
-    the ranks of ``group`` (one process per GPU): per pivot block the owning
-    rank computes the pivot tile and the row panel, every rank receives the
-    packed row-panel snapshots (b x n), and every rank updates its own rows.
+    the ranks of ``group`` (one process per GPU), with the single-GPU
+    lookahead: pivot blocks go in groups of up to 8 (4-byte storage) inside
+    one rank's slab (fw_groups); per group the owner runs the pivot tiles and
+    row panels of all its blocks, every rank receives the group's pivot-row
+    snapshots and packed row-panel snapshots once, computes its column panels
+    and updates its rows with the whole group in one GEMM pass (K = 8b).
 
     On NCCL groups the panel distribution is **fused into the owner's
-    kernels**: the workspaces live in symmetric memory and the phase-1 /
-    row-panel kernels store every snapshot into the peers' broadcast regions
-    as they produce it (btas_fw_dist_stage_peers); a one-word all-reduce then
-    orders the peers' column panels after it, and two workspaces alternate by
-    pivot-block parity so the next owner never overwrites a region a peer is
+    kernels**: the workspaces live in symmetric memory and the owner's
+    kernels store every snapshot into the peers' broadcast regions as they
+    produce it (btas_fw_dist_group_peers); a one-word all-reduce per group
+    then orders the peers' REST stage after it, and two workspaces alternate
+    by group parity so the next owner never overwrites a region a peer is
     still reading.  Otherwise (``BTAS_EXCHANGE=nccl``, no symmetric memory)
-    the owner's region goes out with one NCCL broadcast per block.
+    the owner's region goes out with one NCCL broadcast per group.
     ``peer_workspaces(nbytes, device, group, world)`` may replace the
     symmetric-memory allocation (multi-process tests on one GPU map the
     workspaces with CUDA IPC).  Every rank passes the same adjacency and
@@ -585,7 +594,8 @@ def floyd_warshall_distributed(adj, group=None, peer_workspaces=None):
     rk, peer_ptrs = None, None
     if fused:
         probe = _FwRank(rank, r0, r1 - r0, d[r0:r1], code, n, dev, nbuf=0)
-        got = (peer_workspaces or _fw_peer_workspaces)(probe.total, dev, group, world)
+        got = (peer_workspaces(probe.total, dev, group, world) if peer_workspaces is not None
+               else _peer_buffers((probe.total,), torch.uint8, dev, group, world))
         ok = torch.tensor([1 if got is not None else 0], dtype=torch.int32, device=dev)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)  # every rank takes the same route
         if int(_host_read(ok)[0]) and got is not None:
@@ -599,14 +609,14 @@ def floyd_warshall_distributed(adj, group=None, peer_workspaces=None):
     if peer_ptrs is not None:
         token = torch.zeros(1, dtype=torch.int32, device=dev)
 
-        def bcast(owner, ranks, kb):  # the owner's kernels already stored the panel into the peers
+        def bcast(owner, ranks, gi):  # the owner's kernels already stored the panels into the peers
             dist.all_reduce(token, op=dist.ReduceOp.MAX, group=group)
 
-        def peers(kb, r):
-            return peer_ptrs[kb % 2]
+        def peers(gi, r):
+            return peer_ptrs[gi % 2]
     else:
-        def bcast(owner, ranks, kb):
-            dist.broadcast(ranks[0].region(kb), src=dist.get_global_rank(group, owner) if group is not None else owner,
+        def bcast(owner, ranks, gi):
+            dist.broadcast(ranks[0].region(gi), src=dist.get_global_rank(group, owner) if group is not None else owner,
                            group=group)
 
         peers = None
@@ -630,7 +640,7 @@ def floyd_warshall_emulated(adj, world: int, fused: bool = False):
     """The row-sharded program of ``floyd_warshall_distributed`` with
     ``world`` virtual ranks executed in sequence on ONE GPU (slabs are row
     ranges of one matrix).  ``fused=False``: the broadcast is a device copy;
-    ``fused=True``: the owner's PIVOT kernels store the panel into the other
+    ``fused=True``: the owner's OWNER-stage kernels store the panels into the other
     virtual ranks' (double-buffered) workspaces at exactly the addresses the
     multi-GPU path uses.  The result must equal the single-GPU solve."""
     from .semiring import _note_saturation
@@ -647,17 +657,17 @@ def floyd_warshall_emulated(adj, world: int, fused: bool = False):
     ranks = [_FwRank(r, r0, r1 - r0, d[r0:r1], code, n, d.device, nbuf=nbuf) for r, (r0, r1) in enumerate(spans)]
 
     if fused:
-        def bcast(owner, rks, kb):
+        def bcast(owner, rks, gi):
             pass
 
-        def peers(kb, r):
-            return [rk.region(kb).data_ptr() for rk in ranks if rk.rank != r]
+        def peers(gi, r):
+            return [rk.region(gi).data_ptr() for rk in ranks if rk.rank != r]
     else:
-        def bcast(owner, rks, kb):
-            src = rks[owner].region(kb)
+        def bcast(owner, rks, gi):
+            src = rks[owner].region(gi)
             for rk in rks:
                 if rk.rank != owner:
-                    rk.region(kb).copy_(src)
+                    rk.region(gi).copy_(src)
 
         peers = None
 

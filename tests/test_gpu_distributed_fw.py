@@ -1,4 +1,4 @@
-"""Row-sharded Floyd-Warshall (pivot-panel broadcast, btas_fw_dist_stage).
+"""Row-sharded Floyd-Warshall (lookahead groups, btas_fw_dist_group).
 
 Only one GPU is available to this build, so P > 1 runs as virtual ranks
 executed in sequence on one device (the broadcast becomes a device copy) —
@@ -26,8 +26,8 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.parametrize("world", [1, 2, 3, 5])
 @pytest.mark.parametrize("fused", [False, True])
 def test_emulated_ranks_match_single_gpu(cuda, dtype, world, fused):
-    """fused=True: the owner's PIVOT kernels store the panel straight into the
-    other virtual ranks' double-buffered workspaces (btas_fw_dist_stage_peers)."""
+    """fused=True: the owner's OWNER-stage kernels store the panels straight into the
+    other virtual ranks' double-buffered workspaces (btas_fw_dist_group_peers)."""
     for n, p, wr, seed in ((700, 0.5, (1, 100), 1), (333, 0.05, (0, 60), 2), (130, 0.4, (-1, 40), 3), (1, 0.5, (1, 2), 4)):
         adj = random_graph_matrix(n, p, wr, seed, dtype=dtype)
         want = bt.floyd_warshall(adj)
@@ -35,6 +35,18 @@ def test_emulated_ranks_match_single_gpu(cuda, dtype, world, fused):
         assert got.negative_cycle == want.negative_cycle
         if not want.negative_cycle:
             assert got.distances.dist == want.distances.dist, (n, world)
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_emulated_groups_larger_graphs(cuda, world):
+    """Slabs of many pivot blocks: full lookahead groups of 8 plus ragged
+    tails inside each slab (n = 2500 and 8192), both distributions."""
+    for n, dtype in ((2500, torch.int32), (8192, torch.int32), (2500, torch.float32)):
+        adj = random_graph_matrix(n, 0.5, (1, 100), 77 + n, dtype=dtype)
+        want = bt.floyd_warshall(adj)
+        for fused in (False, True):
+            got = floyd_warshall_emulated(adj, world, fused=fused)
+            assert got.distances.dist == want.distances.dist and not got.negative_cycle, (n, world, fused)
 
 
 def test_emulated_negative_cycles_and_masked(cuda, golden):

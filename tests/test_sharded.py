@@ -138,3 +138,19 @@ def test_sharded_matmul_gloo_world2():
             for rank in range(world):
                 got, gsat = results[(rank, idx, acc)]
                 assert got == want.tobytes() and gsat == sat, (idx, acc, rank)
+
+
+def test_fw_groups_never_span_slabs():
+    from paper_1701_04733_b200.sharded import fw_groups
+
+    for n, world in ((65536, 8), (32768, 3), (1000, 2), (129, 2), (1, 1), (4097, 5)):
+        chunk, spans = partition(n, world)
+        groups = fw_groups(n, 128, chunk, 8)
+        kb = 0
+        for kb0, m, owner in groups:
+            assert kb0 == kb and 1 <= m <= 8
+            r0, r1 = spans[owner]
+            assert r0 <= kb0 * 128 < r1 and min(n, (kb0 + m) * 128) <= r1
+            kb += m
+        assert kb == -(-n // 128)
+    assert len(fw_groups(65536, 128, 8192, 8)) == 64

@@ -1,6 +1,6 @@
 """floyd_warshall_distributed across real processes: 2-3 processes on ONE GPU,
 gloo for the collectives, both panel distributions: the broadcast, and the
-fused one where the owner's PIVOT kernels store the panel into the other
+fused one where the owner's OWNER-stage kernels store the panels into the other
 processes' workspaces (mapped with CUDA IPC).  Every wait is host-mediated,
 so no kernel waits on another process's kernel.  Checked against the
 single-process solve."""
