@@ -251,3 +251,23 @@ def closure_rows(adj: np.ndarray, rows, storage: str = "f64", integer: bool = Fa
             return r
         r = nxt
     raise RuntimeError("closure rows did not converge (negative cycle?)")
+
+
+def predecessors(adj: np.ndarray, dist: np.ndarray) -> np.ndarray:
+    """Predecessor matrix restated (the GPU extension's definition; the
+    reference has no path output): P[i, j] = the smallest k != j with
+    dist[i, k] + adj[k, j] == dist[i, j], -1 if i == j or none / infinite.
+    Oriented min-plus float64 inputs, exact integer weights."""
+    n = adj.shape[0]
+    a = np.array(adj, dtype=np.float64)
+    np.fill_diagonal(a, math.inf)
+    out = np.full((n, n), -1, dtype=np.int32)
+    for i in range(n):
+        with np.errstate(invalid="ignore"):
+            cand = dist[i][:, None] + a  # [k, j]
+        best = cand.min(axis=0)
+        k = np.argmin(cand, axis=0)  # first minimum
+        ok = np.isfinite(best) & (best == dist[i])
+        ok[i] = False
+        out[i, ok] = k[ok]
+    return out

@@ -162,3 +162,29 @@ extern "C" int btas_gemm_peers(int dtype, int kind, int integer_mode, const void
   return gemm_entry(dtype, kind, integer_mode, A, lda, B, ldb, nullptr, 0, C, ldc, M, N, K, Cprev, ldcp, dev_flags,
                     workspace, workspace_bytes, x, stream);
 }
+
+extern "C" int btas_gemm_argmin(int dtype, const void* A, int64_t lda, const void* B, int64_t ldb, const void* Cref,
+                                int64_t ldcr, int64_t M, int64_t N, int64_t K, int64_t row0, int32_t* idx, int64_t ldi,
+                                void* workspace, size_t workspace_bytes, btas_stream_t stream) {
+  if (!A || !B || !Cref || !idx || !workspace || M < 1 || N < 1 || K < 1 || lda < K || ldb < N || ldcr < N ||
+      ldi < N || row0 < 0)
+    return BTAS_ERR_INVALID;
+  if (K > 0x7FFFFFFFLL) return BTAS_ERR_UNSUPPORTED;
+  if ((int64_t)ceil_div(M, 32) > 65535) return BTAS_ERR_UNSUPPORTED;
+  if (workspace_bytes < gemm_ws_total(dtype, M, N, K)) return BTAS_ERR_WORKSPACE;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  unsigned char* ws = static_cast<unsigned char*>(workspace);
+  switch (dtype) {
+    case BTAS_F32:
+      return argmin_f32((const float*)A, lda, (const float*)B, ldb, (const float*)Cref, ldcr, M, N, K, row0, idx, ldi,
+                        ws, st);
+    case BTAS_I32:
+      return argmin_i32((const int32_t*)A, lda, (const int32_t*)B, ldb, (const int32_t*)Cref, ldcr, M, N, K, row0,
+                        idx, ldi, ws, st);
+    case BTAS_F64:
+      return argmin_f64((const double*)A, lda, (const double*)B, ldb, (const double*)Cref, ldcr, M, N, K, row0, idx,
+                        ldi, ws, st);
+    default:
+      return BTAS_ERR_INVALID;
+  }
+}

@@ -70,6 +70,7 @@ struct GemmArgs {
   // storing C; smallest violating row-major index -> *first_bad
   unsigned long long* first_bad;
   int verify_mode;       // BTAS_VERIFY_LE / BTAS_VERIFY_EQ
+  int64_t arg_row0;      // predecessor product: global row of output row 0 (i == j test)
 };
 
 // per-call options of the btas_gemm drivers beyond the plain product
@@ -91,6 +92,7 @@ struct MixF32 {
   static constexpr int GM = 4, GN = 4, KP = 16, STAGES = 4;
   static constexpr int path = BTAS_PATH_FAST32;
   static constexpr bool kChecked = false;
+  static constexpr bool kArg = false;
   BTAS_D static Acc init() { return MIN ? INFINITY : -INFINITY; }
   BTAS_D static void step(Acc& c, E a0, E a1, E b0, E b1, bool&, const GemmArgs&) {
     float2 s = __fadd2_rn(make_float2(a0, a1), make_float2(b0, b1));
@@ -112,6 +114,7 @@ struct MixI32 {
   static constexpr int GM = 4, GN = 4, KP = 16, STAGES = 4;
   static constexpr int path = BTAS_PATH_FAST32;
   static constexpr bool kChecked = false;
+  static constexpr bool kArg = false;
   BTAS_D static Acc init() { return MIN ? kI32Inf : -kI32Inf; }
   BTAS_D static void step(Acc& c, E a0, E a1, E b0, E b1, bool&, const GemmArgs&) {
     if (MIN) {
@@ -145,6 +148,7 @@ struct MixI32F64 {
   static constexpr int GM = 4, GN = 4, KP = 16, STAGES = 4;
   static constexpr int path = BTAS_PATH_I32F64;
   static constexpr bool kChecked = false;
+  static constexpr bool kArg = false;
   BTAS_D static Acc init() { return MIN ? kI32Inf : -kI32Inf; }
   BTAS_D static void step(Acc& c, E a0, E a1, E b0, E b1, bool&, const GemmArgs&) {
     if (MIN) {
@@ -169,6 +173,7 @@ struct MixF64 {
   static constexpr int GM = 2, GN = 4, KP = 16, STAGES = 3;
   static constexpr int path = BTAS_PATH_FAST64;
   static constexpr bool kChecked = false;
+  static constexpr bool kArg = false;
   BTAS_D static Acc init() { return MIN ? INFINITY : -INFINITY; }
   BTAS_D static void step(Acc& c, E a0, E a1, E b0, E b1, bool&, const GemmArgs&) {
     double s0 = __dadd_rn(a0, b0), s1 = __dadd_rn(a1, b1);
@@ -192,6 +197,7 @@ struct MixS16 {
   static constexpr int GM = 4, GN = GNv, KP = 16, STAGES = 4;
   static constexpr int path = BTAS_PATH_S16X2;
   static constexpr bool kChecked = false;
+  static constexpr bool kArg = false;
   BTAS_D static Acc init() {
     const uint32_t inf = MIN ? (uint32_t)kS16Inf : (uint32_t)(uint16_t)(-kS16Inf);
     return inf | (inf << 16);
@@ -225,6 +231,7 @@ struct MixChecked {
   static constexpr int GM = sizeof(T) == 8 ? 2 : 4, GN = 4, KP = 16, STAGES = sizeof(T) == 8 ? 3 : 4;
   static constexpr int path = BTAS_PATH_CHECKED;
   static constexpr bool kChecked = true;
+  static constexpr bool kArg = false;
   BTAS_D static Acc init() { return Traits<T>::eps(MIN); }
   BTAS_D static T cand(T a, T b, bool& sat, const GemmArgs& g) {
     T s = a + b;
@@ -257,6 +264,42 @@ struct MixChecked {
       if (MIN) return c >= (T)kI32Limit ? (T)kI32Inf : c;
       return c <= -(T)kI32Limit ? (T)(-kI32Inf) : c;
     }
+    return c;
+  }
+};
+
+// Predecessor product (path reconstruction): the
+// min-plus product A (x) B together with, per output, the FIRST k attaining
+// the minimum (strict < in increasing k; the k dimension is never split, so
+// the index is deterministic).  Used as D (x) (A with an infinite diagonal):
+// the argmin is the last hop of a shortest path.  The epilogue writes int32
+// indices (-1 where the minimum does not reproduce Cprev, the distances).
+template <class T>
+struct MixArg {
+  using E = T;
+  using Acc = T;
+  using Out = T;
+  static constexpr int GM = sizeof(T) == 8 ? 2 : 4, GN = 4, KP = 16, STAGES = sizeof(T) == 8 ? 3 : 4;
+  static constexpr int path = BTAS_PATH_CHECKED;  // never gated
+  static constexpr bool kChecked = false;
+  static constexpr bool kArg = true;
+  BTAS_D static Acc init() { return Traits<T>::eps(true); }
+  BTAS_D static void step_arg(Acc& c, int32_t& idx, E a0, E a1, E b0, E b1, int32_t k0) {
+    // int32 storage: Inf = 2^30-1, sums of two stay below 2^31 and every sum
+    // involving Inf stays >= 2^29 > every finite value
+    const T s0 = a0 + b0, s1 = a1 + b1;
+    if (s0 < c) {
+      c = s0;
+      idx = k0;
+    }
+    if (s1 < c) {
+      c = s1;
+      idx = k0 + 1;
+    }
+  }
+  BTAS_D static void step(Acc&, E, E, E, E, bool&, const GemmArgs&) {}
+  BTAS_D static Out finish(Acc c, const GemmArgs&) {
+    if constexpr (Traits<T>::dtype == BTAS_I32) return c >= (T)kI32Limit ? (T)kI32Inf : c;
     return c;
   }
 };
@@ -464,6 +507,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
     }
 
     Acc acc[GM][2][GN][2];
+    int32_t aidx[P::kArg ? GM : 1][2][P::kArg ? GN : 1][2];  // argmin k (predecessor product only)
 #pragma unroll
     for (int i = 0; i < GM; ++i)
 #pragma unroll
@@ -471,7 +515,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
 #pragma unroll
         for (int j = 0; j < GN; ++j)
 #pragma unroll
-          for (int c = 0; c < 2; ++c) acc[i][r][j][c] = P::init();
+          for (int c = 0; c < 2; ++c) {
+            acc[i][r][j][c] = P::init();
+            if constexpr (P::kArg) aidx[i][r][j][c] = -1;
+          }
 
     for (int kb = 0; kb < nkb; ++kb, ++it) {
       const int s = it % ST;
@@ -492,8 +539,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
 #pragma unroll
             for (int j = 0; j < GN; ++j)
 #pragma unroll
-              for (int c = 0; c < 2; ++c)
-                P::step(acc[i][r][j][c], a[i][2 * r], a[i][2 * r + 1], b[j][2 * c], b[j][2 * c + 1], sat, g);
+              for (int c = 0; c < 2; ++c) {
+                if constexpr (P::kArg)
+                  P::step_arg(acc[i][r][j][c], aidx[i][r][j][c], a[i][2 * r], a[i][2 * r + 1], b[j][2 * c],
+                              b[j][2 * c + 1], (int32_t)(2 * ((int64_t)kb * KP + kp)));
+                else
+                  P::step(acc[i][r][j][c], a[i][2 * r], a[i][2 * r + 1], b[j][2 * c], b[j][2 * c + 1], sat, g);
+              }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
@@ -505,6 +557,29 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
     // only on diagonal tiles.  Edge tiles: two passes (all loads, then all
     // stores — C may alias Z in Floyd-Warshall, so interleaving them would
     // serialise each load's latency).
+    if constexpr (P::kArg) {
+      // predecessor product: C holds int32 indices; Cprev the distances
+      int32_t* Ci = static_cast<int32_t*>(g.C);
+#pragma unroll
+      for (int i = 0; i < GM; ++i)
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int64_t row = (int64_t)mb * BM + i * 32 + ty * 2 + r;
+          if (row >= g.M) continue;
+#pragma unroll
+          for (int j = 0; j < GN; ++j)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              const int64_t col = (int64_t)nb * BN + j * 32 + tx * 2 + c;
+              if (col >= g.N) continue;
+              const Out v = P::finish(acc[i][r][j][c], g);
+              const Out d = Cp[row * g.ldcp + col];
+              const bool tight = Traits<Out>::finite(v) && !bits_differ(v, d) && row + g.arg_row0 != col;
+              Ci[row * g.ldc + col] = tight ? aidx[i][r][j][c] : -1;
+            }
+        }
+      continue;
+    }
     if (interior) {
       const bool diag_tile = !g.no_diag && (int64_t)mb * BM < (int64_t)(nb + 1) * BN &&
                              (int64_t)nb * BN < (int64_t)(mb + 1) * BM;

@@ -467,6 +467,42 @@ int gemm_typed(int integer_mode, const T* A, int64_t lda, const T* B, int64_t ld
 }
 
 
+// predecessor product (MixArg): pack A and B (no screen, no gating: the
+// operands are min-plus distances / adjacency whose sums the caller bounds)
+// and run the argmin kernel; idx receives int32 k indices
+template <class T>
+int argmin_typed(const T* A, int64_t lda, const T* B, int64_t ldb, const T* Cref, int64_t ldcr, int64_t M, int64_t N,
+                 int64_t K, int64_t row0, int32_t* idx, int64_t ldi, unsigned char* ws, const WsLayout& L,
+                 cudaStream_t st) {
+  using G = GemmGeometry<T>;
+  using P = MixArg<T>;
+  static_assert(P::GM * 32 == G::BM, "argmin tiles use the 32/64-bit packed geometry");
+  const int64_t Kp2 = round_up(K, 2 * kKP) / 2;
+  const int64_t Mp = round_up(M, G::BM), Np = round_up(N, G::BN);
+  T* Ap = reinterpret_cast<T*>(ws + L.packA);
+  T* Bp = reinterpret_cast<T*>(ws + L.packB);
+  dim3 ga((unsigned)ceil_div(2 * Kp2, 64), (unsigned)ceil_div(Mp, 32));
+  pack_a_kernel<T, T, false, true, G::BM><<<ga, 256, 0, st>>>(A, lda, M, K, 2 * Kp2, Kp2, Ap, nullptr, 0, 0);
+  const int64_t tb = Kp2 * Np;
+  pack_b_kernel<T, T, false, true, G::BN><<<(unsigned)std::min<int64_t>(ceil_div(tb, 256), 65535), 256, 0, st>>>(
+      B, ldb, K, N, Np, Kp2, Bp, nullptr, 0, 0);
+  BTAS_CUDA_CHECK_LAUNCH();
+  GemmArgs g{};
+  g.Ap = Ap;
+  g.Bp = Bp;
+  g.Kp2 = Kp2;
+  g.M = M;
+  g.N = N;
+  g.mblocks = (int)(Mp / G::BM);
+  g.nblocks = (int)(Np / G::BN);
+  g.C = idx;
+  g.ldc = ldi;
+  g.Cprev = Cref;
+  g.ldcp = ldcr;
+  g.arg_row0 = row0;
+  return launch_gemm_epi<P, true, kEpiCmp>(g, st);
+}
+
 }  // namespace
 }  // namespace gemm_impl
 
@@ -488,5 +524,11 @@ BTAS_GEMM_HALF_DECL(float, gemm_f32_max);
 BTAS_GEMM_HALF_DECL(int32_t, gemm_i32_max);
 BTAS_GEMM_HALF_DECL(double, gemm_f64_max);
 size_t gemm_ws_total(int dtype, int64_t M, int64_t N, int64_t K);
+#define BTAS_ARGMIN_DECL(T, NAME)                                                                                \
+  int NAME(const T* A, int64_t lda, const T* B, int64_t ldb, const T* Cref, int64_t ldcr, int64_t M, int64_t N,    \
+           int64_t K, int64_t row0, int32_t* idx, int64_t ldi, unsigned char* ws, cudaStream_t st)
+BTAS_ARGMIN_DECL(float, argmin_f32);
+BTAS_ARGMIN_DECL(int32_t, argmin_i32);
+BTAS_ARGMIN_DECL(double, argmin_f64);
 
 }  // namespace btas

@@ -1,0 +1,74 @@
+"""Path reconstruction (an extension — the reference
+returns distances only): the predecessor product (btas_gemm_argmin) against
+the oracle's definition, and shortest paths walked from it reproduce the
+distances."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1701_04733_b200 as bt
+from paper_1701_04733_b200.graphs import dense_rows, random_graph_matrix
+from oracle import tropical as ot
+
+from gpu_helpers import DTYPES, MIN, symbolic
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_predecessors_match_oracle(cuda, dtype):
+    for n, p, wr, seed in ((1, 0.5, (1, 9), 1), (2, 1.0, (1, 9), 2), (37, 0.3, (0, 5), 3), (130, 0.1, (1, 100), 4),
+                           (300, 0.5, (1, 3), 5), (257, 0.02, (0, 20), 6)):
+        adj = random_graph_matrix(n, p, wr, seed, dtype=dtype)
+        rep = bt.floyd_warshall(adj)
+        pred = bt.predecessors(adj, rep)
+        sym = np.concatenate([b for _, b in dense_rows(n, p, wr, seed)])
+        want = ot.predecessors(ot.orient(ot.MIN, sym), rep.distances.dist.to_numpy())
+        assert np.array_equal(pred.cpu().numpy(), want), (n, p, wr)
+        assert bt.predecessors(adj, bt.apsp_by_squaring(adj)).equal(pred)
+
+
+@pytest.mark.parametrize("dtype", [torch.int32, torch.float32])
+def test_shortest_paths_reproduce_distances(cuda, dtype):
+    """Positive weights: every walked path exists edge by edge and its weight
+    is the distance (n = 2000, 300 sampled pairs incl. unreachable ones)."""
+    n = 2000
+    adj = random_graph_matrix(n, 0.003, (1, 100), 11, dtype=dtype)
+    rep = bt.floyd_warshall(adj)
+    pred = bt.predecessors(adj, rep)
+    a = adj.to_numpy()
+    d = rep.distances.dist.to_numpy()
+    rng = np.random.default_rng(2)
+    unreachable = 0
+    for i, j in rng.integers(0, n, (300, 2)):
+        path = bt.shortest_path(pred, int(i), int(j))
+        if path is None:
+            assert math.isinf(d[i, j])
+            unreachable += 1
+            continue
+        assert path[0] == i and path[-1] == j and len(path) <= n
+        w = sum(a[u, v] for u, v in zip(path, path[1:]))
+        assert w == d[i, j], (i, j)
+    assert 0 < unreachable < 300
+    with pytest.raises(ValueError):
+        bt.predecessors(bt.TropicalMatrix(MIN, [[0, -2], [1, 0]]))
+
+
+def test_predecessors_at_scale(cuda):
+    """n = 16384 int32 (the C2 size): path weights equal the distances on
+    sampled pairs; the product runs through the tiled argmin GEMM."""
+    n = 16384
+    adj = random_graph_matrix(n, 0.5, (1, 100), 99, dtype=torch.int32)
+    rep = bt.floyd_warshall(adj)
+    pred = bt.predecessors(adj, rep)
+    d = rep.distances.dist.data
+    a = adj.data
+    rng = np.random.default_rng(3)
+    for i, j in rng.integers(0, n, (64, 2)):
+        path = bt.shortest_path(pred, int(i), int(j))
+        w = sum(int(a[u, v]) for u, v in zip(path, path[1:]))
+        assert w == int(d[i, j])
+    assert int((pred < 0).sum()) == n  # only the diagonal: the graph is strongly connected
