@@ -36,7 +36,7 @@ def test_shortest_paths_reproduce_distances(cuda, dtype):
     """Positive weights: every walked path exists edge by edge and its weight
     is the distance (n = 2000, 300 sampled pairs incl. unreachable ones)."""
     n = 2000
-    adj = random_graph_matrix(n, 0.003, (1, 100), 11, dtype=dtype)
+    adj = random_graph_matrix(n, 0.001, (1, 100), 11, dtype=dtype)
     rep = bt.floyd_warshall(adj)
     pred = bt.predecessors(adj, rep)
     a = adj.to_numpy()
