@@ -295,7 +295,7 @@ int btas_diag_negative(int dtype, const void* d, int64_t ld, int64_t n, int32_t*
 
 /* Register/shared-memory microbenchmark of the add-min instruction mixes
  * (the roofline denominator).  mix: 0 = f32 FADD2+FMNMX3, 1 = i32 VIADDMNMX,
- * 2 = s16x2 VIADDMNMX.S16x2.  Writes pairs per SM clock and the effective
+ * 2 = s16x2 VIADDMNMX.S16x2, 3 = f64 DADD + ternary compare (DSETP + FSEL).  Writes pairs per SM clock and the effective
  * SM clock (MHz) of the run.  Synchronises (diagnostic only). */
 int btas_probe_ceiling(int mix, double* pairs_per_clk_sm, double* sm_mhz, double* tpairs_per_s);
 

@@ -16,6 +16,87 @@ namespace {
 
 constexpr int kProbeIters = 8192;
 
+// f64 (mix 3): the MixF64 step — DADD over a k pair, two ternary compares —
+// on a 4 x 4 double microtile with register operands (the FP64 compare is the
+// limiter, not shared memory)
+__global__ void __launch_bounds__(256) probe_f64_kernel(const double* __restrict__ gin, double* gout,
+                                                        long long* cycles) {
+  double a[4][2], b[4][2], acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    a[i][0] = gin[(threadIdx.x + i) & 255];
+    a[i][1] = gin[(threadIdx.x + 3 * i + 1) & 255];
+    b[i][0] = gin[(threadIdx.x * 7 + i) & 255];
+    b[i][1] = gin[(threadIdx.x * 5 + i + 9) & 255];
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 1e300;
+  const long long t0 = clock64();
+  for (int it = 0; it < kProbeIters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double s0 = __dadd_rn(a[i][0], b[j][0]), s1 = __dadd_rn(a[i][1], b[j][1]);
+        double& c = acc[i][j];
+        c = s0 < c ? s0 : c;
+        c = s1 < c ? s1 : c;
+      }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i][0] += 1.0;
+  }
+  const long long t1 = clock64();
+  double r = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) r += acc[i][j];
+  gout[blockIdx.x * blockDim.x + threadIdx.x] = r;
+  if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
+}
+
+int run_probe_f64(double* ppc, double* mhz, double* tps) {
+  const int nsm = device_sm_count();
+  double *din = nullptr, *dout = nullptr;
+  long long* dcyc = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  int rc = BTAS_ERR_CUDA;
+  std::vector<double> h(256);
+  std::vector<long long> hc(nsm);
+  for (int i = 0; i < 256; ++i) h[i] = 1.0 + (i * 37 % 101) * 0.37;
+  if (cudaMalloc(&din, 256 * 8) || cudaMalloc(&dout, (size_t)nsm * 256 * 8) || cudaMalloc(&dcyc, nsm * 8)) goto done;
+  if (cudaMemcpy(din, h.data(), 256 * 8, cudaMemcpyHostToDevice)) goto done;
+  probe_f64_kernel<<<nsm, 256>>>(din, dout, dcyc);
+  if (cudaDeviceSynchronize()) goto done;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  probe_f64_kernel<<<nsm, 256>>>(din, dout, dcyc);
+  cudaEventRecord(e1);
+  if (cudaEventSynchronize(e1)) goto done;
+  {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (cudaMemcpy(hc.data(), dcyc, nsm * 8, cudaMemcpyDeviceToHost)) goto done;
+    const long long mx = *std::max_element(hc.begin(), hc.end());
+    const double pairs = 32.0 * kProbeIters * 256.0 * nsm;
+    *ppc = pairs / nsm / (double)mx;
+    *mhz = (double)mx / (ms * 1e-3) / 1e6;
+    *tps = pairs / (ms * 1e-3) / 1e12;
+    rc = BTAS_OK;
+  }
+done:
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  cudaFree(din);
+  cudaFree(dout);
+  cudaFree(dcyc);
+  (void)cudaGetLastError();
+  return rc;
+}
+
 template <int MIX>
 __global__ void __launch_bounds__(256) probe_kernel(const uint32_t* __restrict__ gin, uint32_t* gout,
                                                     long long* cycles) {
@@ -114,6 +195,8 @@ extern "C" int btas_probe_ceiling(int mix, double* pairs_per_clk_sm, double* sm_
       return btas::run_probe<1>(pairs_per_clk_sm, sm_mhz, tpairs_per_s);
     case 2:
       return btas::run_probe<2>(pairs_per_clk_sm, sm_mhz, tpairs_per_s);
+    case 3:
+      return btas::run_probe_f64(pairs_per_clk_sm, sm_mhz, tpairs_per_s);
     default:
       return BTAS_ERR_INVALID;
   }
