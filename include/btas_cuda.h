@@ -189,11 +189,15 @@ int btas_gemm_verify(int dtype, int kind, int integer_mode,
  * minimum is not finite, differs from Cref[i,j], or row0 + i == j.  With A =
  * the distance matrix, B = the adjacency with an infinite diagonal and Cref =
  * the distances, idx is the last hop of a shortest path (the predecessor
- * matrix).  Same workspace as btas_gemm (btas_gemm_workspace_bytes). */
-int btas_gemm_argmin(int dtype, const void* A, int64_t lda, const void* B, int64_t ldb,
-                     const void* Cref, int64_t ldcr, int64_t M, int64_t N, int64_t K, int64_t row0,
-                     int32_t* idx, int64_t ldi, void* workspace, size_t workspace_bytes,
-                     btas_stream_t stream);
+ * matrix).  Same workspace as btas_gemm (btas_gemm_workspace_bytes).
+ * operand_bound >= max |finite entry| of A and of B (negative: unknown):
+ * integer data (int32, or integer_mode) below 2^12 with K <= 65536 runs as
+ * packed (value << 16 | k) keys through the VIADDMNMX kernel (one
+ * instruction per candidate); otherwise compare-and-select per candidate. */
+int btas_gemm_argmin(int dtype, int integer_mode, double operand_bound, const void* A, int64_t lda,
+                     const void* B, int64_t ldb, const void* Cref, int64_t ldcr, int64_t M, int64_t N,
+                     int64_t K, int64_t row0, int32_t* idx, int64_t ldi, void* workspace,
+                     size_t workspace_bytes, btas_stream_t stream);
 
 /* Elementwise half of find_apsp_violation (apsp.py:194-200) in one pass over
  * D and the adjacency A (n x n, same storage): first[0] <- smallest i with

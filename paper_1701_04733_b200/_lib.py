@@ -115,7 +115,8 @@ SIGNATURES = {
         [_i32, _i32, _i32, _p, _i64, _p, _i64, _p, _i64, _i64, _i64, _i64, _i32, _p, _p, _p, _sz, _p],
     ),
     "btas_verify_base": (_i32, [_i32, _p, _i64, _p, _i64, _i64, _p, _p]),
-    "btas_gemm_argmin": (_i32, [_i32, _p, _i64, _p, _i64, _p, _i64, _i64, _i64, _i64, _i64, _p, _i64, _p, _sz, _p]),
+    "btas_gemm_argmin": (_i32, [_i32, _i32, _dbl, _p, _i64, _p, _i64, _p, _i64, _i64, _i64, _i64, _i64, _p, _i64, _p,
+                                _sz, _p]),
     "btas_gemm_timing": (_i32, [_i32]),
     "btas_gemm_timing_read": (_i32, [ctypes.POINTER(_dbl), ctypes.POINTER(_i32)]),
     "btas_matvec": (_i32, [_i32, _i32, _i32, _p, _i64, _i64, _i64, _p, _i64, _i64, _p, _i64, _p, _p]),

@@ -163,9 +163,10 @@ extern "C" int btas_gemm_peers(int dtype, int kind, int integer_mode, const void
                     workspace, workspace_bytes, x, stream);
 }
 
-extern "C" int btas_gemm_argmin(int dtype, const void* A, int64_t lda, const void* B, int64_t ldb, const void* Cref,
-                                int64_t ldcr, int64_t M, int64_t N, int64_t K, int64_t row0, int32_t* idx, int64_t ldi,
-                                void* workspace, size_t workspace_bytes, btas_stream_t stream) {
+extern "C" int btas_gemm_argmin(int dtype, int integer_mode, double operand_bound, const void* A, int64_t lda,
+                                const void* B, int64_t ldb, const void* Cref, int64_t ldcr, int64_t M, int64_t N,
+                                int64_t K, int64_t row0, int32_t* idx, int64_t ldi, void* workspace,
+                                size_t workspace_bytes, btas_stream_t stream) {
   if (!A || !B || !Cref || !idx || !workspace || M < 1 || N < 1 || K < 1 || lda < K || ldb < N || ldcr < N ||
       ldi < N || row0 < 0)
     return BTAS_ERR_INVALID;
@@ -174,16 +175,20 @@ extern "C" int btas_gemm_argmin(int dtype, const void* A, int64_t lda, const voi
   if (workspace_bytes < gemm_ws_total(dtype, M, N, K)) return BTAS_ERR_WORKSPACE;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   unsigned char* ws = static_cast<unsigned char*>(workspace);
+  // (value, k) keys when every finite operand is an integer below 2^12 in
+  // magnitude (then every finite sum key stays below 2^29) and k fits 16 bits
+  const bool keys = (dtype == BTAS_I32 || integer_mode) && operand_bound >= 0.0 &&
+                    operand_bound < (double)kS16Limit && K <= 65536;
   switch (dtype) {
     case BTAS_F32:
       return argmin_f32((const float*)A, lda, (const float*)B, ldb, (const float*)Cref, ldcr, M, N, K, row0, idx, ldi,
-                        ws, st);
+                        keys, ws, st);
     case BTAS_I32:
       return argmin_i32((const int32_t*)A, lda, (const int32_t*)B, ldb, (const int32_t*)Cref, ldcr, M, N, K, row0,
-                        idx, ldi, ws, st);
+                        idx, ldi, keys, ws, st);
     case BTAS_F64:
       return argmin_f64((const double*)A, lda, (const double*)B, ldb, (const double*)Cref, ldcr, M, N, K, row0, idx,
-                        ldi, ws, st);
+                        ldi, keys, ws, st);
     default:
       return BTAS_ERR_INVALID;
   }

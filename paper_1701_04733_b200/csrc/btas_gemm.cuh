@@ -313,6 +313,31 @@ struct MixArg {
   }
 };
 
+// The predecessor product for small integer data (|x| < 2^12, K <= 2^16):
+// operands packed as keys  a' = a << 16,  b' = (b << 16) + k  (Inf -> a
+// large key), so  a' + b' = ((a + b) << 16) + k  and one VIADDMNMX per
+// candidate keeps the minimum sum AND, among equal sums, the smallest k — the
+// same first argmin as MixArg at the plain int32 GEMM rate.  Decoded in the
+// epilogue (value = key >> 16, k = key & 0xFFFF).
+template <class T>
+struct MixArgKey {
+  using E = int32_t;
+  using Acc = int32_t;
+  using Out = T;  // Cprev (the distances) is read in the storage type
+  static constexpr int GM = 4, GN = 4, KP = 16, STAGES = 4;
+  static constexpr int path = BTAS_PATH_FAST32;  // never gated
+  static constexpr bool kChecked = false;
+  static constexpr bool kArg = true;
+  static constexpr bool kArgKey = true;
+  BTAS_D static Acc init() { return (1 << 30) - 1; }
+  BTAS_D static void step(Acc& c, E a0, E a1, E b0, E b1, bool&, const GemmArgs&) {
+    c = __viaddmin_s32(a0, b0, c);
+    c = __viaddmin_s32(a1, b1, c);
+  }
+  BTAS_D static void step_arg(Acc&, int32_t&, E, E, E, E, int32_t) {}
+  BTAS_D static Out finish(Acc c, const GemmArgs&) { return (Out)c; }  // unused: the key epilogue decodes
+};
+
 // ---------------------------------------------------------------------------
 // helpers
 // ---------------------------------------------------------------------------
@@ -417,6 +442,11 @@ BTAS_D void verify_entry(const GemmArgs& g, Out v, Out ref, int64_t row, int64_t
   }
 }
 constexpr int kMaxPeers = 7;
+
+template <class P, class = void>
+struct arg_key : std::false_type {};
+template <class P>
+struct arg_key<P, std::void_t<decltype(P::kArgKey)>> : std::bool_constant<P::kArgKey> {};
 
 template <class P, bool MIN, int EPI>
 __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __grid_constant__ GemmArgs g) {
@@ -549,7 +579,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
             for (int j = 0; j < GN; ++j)
 #pragma unroll
               for (int c = 0; c < 2; ++c) {
-                if constexpr (P::kArg)
+                if constexpr (P::kArg && !arg_key<P>::value)
                   P::step_arg(acc[i][r][j][c], aidx[i][r][j][c], a[i][2 * r], a[i][2 * r + 1], b[j][2 * c],
                               b[j][2 * c + 1], (int32_t)(2 * ((int64_t)kb * KP + kp)));
                 else
@@ -581,10 +611,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
             for (int c = 0; c < 2; ++c) {
               const int64_t col = (int64_t)nb * BN + j * 32 + tx * 2 + c;
               if (col >= g.N) continue;
-              const Out v = P::finish(acc[i][r][j][c], g);
               const Out d = Cp[row * g.ldcp + col];
-              const bool tight = Traits<Out>::finite(v) && !bits_differ(v, d) && row + g.arg_row0 != col;
-              Ci[row * g.ldc + col] = tight ? aidx[i][r][j][c] : -1;
+              if constexpr (arg_key<P>::value) {
+                const int32_t key = acc[i][r][j][c];
+                const bool tight = key < (1 << 29) && Traits<Out>::finite(d) && (Out)(key >> 16) == d &&
+                                   row + g.arg_row0 != col;
+                Ci[row * g.ldc + col] = tight ? (key & 0xFFFF) : -1;
+              } else {
+                const Out v = P::finish(acc[i][r][j][c], g);
+                const bool tight = Traits<Out>::finite(v) && !bits_differ(v, d) && row + g.arg_row0 != col;
+                Ci[row * g.ldc + col] = tight ? aidx[i][r][j][c] : -1;
+              }
             }
         }
       continue;

@@ -17,7 +17,7 @@ size_t gemm_ws_total(int dtype, int64_t M, int64_t N, int64_t K) {
 
 BTAS_ARGMIN_DECL(float, argmin_f32) {
   const gemm_impl::WsLayout L = gemm_impl::ws_layout(Traits<float>::dtype, M, N, K);
-  return gemm_impl::argmin_typed<float>(A, lda, B, ldb, Cref, ldcr, M, N, K, row0, idx, ldi, ws, L, st);
+  return gemm_impl::argmin_typed<float>(A, lda, B, ldb, Cref, ldcr, M, N, K, row0, idx, ldi, keys, ws, L, st);
 }
 
 }  // namespace btas

@@ -13,7 +13,7 @@ BTAS_GEMM_DRIVER_DECL(double, gemm_f64) {
 
 BTAS_ARGMIN_DECL(double, argmin_f64) {
   const gemm_impl::WsLayout L = gemm_impl::ws_layout(Traits<double>::dtype, M, N, K);
-  return gemm_impl::argmin_typed<double>(A, lda, B, ldb, Cref, ldcr, M, N, K, row0, idx, ldi, ws, L, st);
+  return gemm_impl::argmin_typed<double>(A, lda, B, ldb, Cref, ldcr, M, N, K, row0, idx, ldi, keys, ws, L, st);
 }
 
 }  // namespace btas

@@ -13,7 +13,7 @@ BTAS_GEMM_DRIVER_DECL(int32_t, gemm_i32) {
 
 BTAS_ARGMIN_DECL(int32_t, argmin_i32) {
   const gemm_impl::WsLayout L = gemm_impl::ws_layout(Traits<int32_t>::dtype, M, N, K);
-  return gemm_impl::argmin_typed<int32_t>(A, lda, B, ldb, Cref, ldcr, M, N, K, row0, idx, ldi, ws, L, st);
+  return gemm_impl::argmin_typed<int32_t>(A, lda, B, ldb, Cref, ldcr, M, N, K, row0, idx, ldi, keys, ws, L, st);
 }
 
 }  // namespace btas

@@ -252,12 +252,22 @@ BTAS_D uint32_t to_s16(T x) {
   return (uint32_t)(uint16_t)(int16_t)v;
 }
 
-template <class T, class E, bool S16, bool MIN>
+// predecessor keys (MixArgKey): value << 16 | k packs a min-plus candidate
+// and its k into one int32, so one VIADDMNMX keeps the first argmin
+constexpr int32_t kArgKeyInf = (1 << 30) - (1 << 17);
+
+template <class T, class E, bool S16, bool MIN, int KEYM = 0>
 BTAS_D E load_virtual(const T* __restrict__ X, int64_t ld, int64_t rows, int64_t cols, int64_t r, int64_t c,
                       bool c_is_k) {
   // c_is_k: virtual column index c is along k (A operand, row r); otherwise
   // the virtual row index r is along k (B operand, column c).
-  if constexpr (!S16 && std::is_integral<E>::value && !std::is_integral<T>::value) {
+  if constexpr (KEYM != 0) {  // 1: A operand value << 16; 2: B operand (value << 16) + k
+    if (!(r < rows && c < cols)) return (E)kArgKeyInf;
+    const T x = X[r * ld + c];
+    if (!Traits<T>::finite(x)) return (E)kArgKeyInf;
+    const int32_t v = (int32_t)x * 65536;
+    return (E)(KEYM == 1 ? v : v + (int32_t)r);
+  } else if constexpr (!S16 && std::is_integral<E>::value && !std::is_integral<T>::value) {
     // float64 integer operands packed as int32 (BTAS_PATH_I32F64)
     const T x = (r < rows && c < cols) ? X[r * ld + c] : Traits<T>::eps(MIN);
     return isfinite(x) ? (E)x : (MIN ? (E)kI32Inf : (E)-kI32Inf);
@@ -281,7 +291,7 @@ BTAS_D E load_virtual(const T* __restrict__ X, int64_t ld, int64_t rows, int64_t
 
 // A (M x K) -> Ap[mb][kp][BM][2] over virtual k (words for s16): a 32 x 64
 // smem transpose so both the row reads and the pair writes are coalesced.
-template <class T, class E, bool S16, bool MIN, int BM>
+template <class T, class E, bool S16, bool MIN, int BM, int KEYM = 0>
 __global__ void pack_a_kernel(const T* __restrict__ A, int64_t lda, int64_t M, int64_t K, int64_t Kv, int64_t Kp2,
                               E* __restrict__ Ap, const Ctrl* ctrl, int gate0, int gate1) {
   if (ctrl != nullptr && ctrl->path != gate0 && ctrl->path != gate1) return;
@@ -291,7 +301,7 @@ __global__ void pack_a_kernel(const T* __restrict__ A, int64_t lda, int64_t M, i
   for (int e = threadIdx.x; e < 32 * 64; e += blockDim.x) {
     const int mr = e >> 6, kc = e & 63;
     const int64_t m = m0 + mr, kv = k0 + kc;
-    tile[mr][kc] = load_virtual<T, E, S16, MIN>(A, lda, M, K, m, kv, true);  // eps past M / K
+    tile[mr][kc] = load_virtual<T, E, S16, MIN, KEYM>(A, lda, M, K, m, kv, true);  // eps past M / K
   }
   __syncthreads();
   // write pairs: 32 kp x 32 m
@@ -307,15 +317,15 @@ __global__ void pack_a_kernel(const T* __restrict__ A, int64_t lda, int64_t M, i
 }
 
 // B (K x N) -> Bp[nb][kp][BN][2]: rows 2kp and 2kp+1 interleaved.
-template <class T, class E, bool S16, bool MIN, int BN>
+template <class T, class E, bool S16, bool MIN, int BN, int KEYM = 0>
 __global__ void pack_b_kernel(const T* __restrict__ B, int64_t ldb, int64_t K, int64_t N, int64_t Np, int64_t Kp2,
                               E* __restrict__ Bp, const Ctrl* ctrl, int gate0, int gate1) {
   if (ctrl != nullptr && ctrl->path != gate0 && ctrl->path != gate1) return;
   const int64_t total = Kp2 * Np;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t kp = e / Np, n = e - kp * Np;
-    const E v0 = load_virtual<T, E, S16, MIN>(B, ldb, K, N, 2 * kp, n, false);
-    const E v1 = load_virtual<T, E, S16, MIN>(B, ldb, K, N, 2 * kp + 1, n, false);
+    const E v0 = load_virtual<T, E, S16, MIN, KEYM>(B, ldb, K, N, 2 * kp, n, false);
+    const E v1 = load_virtual<T, E, S16, MIN, KEYM>(B, ldb, K, N, 2 * kp + 1, n, false);
     const int64_t idx = packed_index(n, 2 * kp, Kp2, BN);
     Bp[idx] = v0;
     Bp[idx + 1] = v1;
@@ -472,8 +482,35 @@ int gemm_typed(int integer_mode, const T* A, int64_t lda, const T* B, int64_t ld
 // and run the argmin kernel; idx receives int32 k indices
 template <class T>
 int argmin_typed(const T* A, int64_t lda, const T* B, int64_t ldb, const T* Cref, int64_t ldcr, int64_t M, int64_t N,
-                 int64_t K, int64_t row0, int32_t* idx, int64_t ldi, unsigned char* ws, const WsLayout& L,
+                 int64_t K, int64_t row0, int32_t* idx, int64_t ldi, bool keys, unsigned char* ws, const WsLayout& L,
                  cudaStream_t st) {
+  if (keys) {  // integer operands |x| < 2^12, K <= 2^16: packed (value, k) keys through VIADDMNMX
+    using PK = MixArgKey<T>;
+    const int64_t Kp2 = round_up(K, 2 * kKP) / 2;
+    const int64_t Mp = round_up(M, 128), Np = round_up(N, 128);
+    int32_t* Ap = reinterpret_cast<int32_t*>(ws + L.packA);
+    int32_t* Bp = reinterpret_cast<int32_t*>(ws + L.packB);
+    dim3 ga((unsigned)ceil_div(2 * Kp2, 64), (unsigned)ceil_div(Mp, 32));
+    pack_a_kernel<T, int32_t, false, true, 128, 1><<<ga, 256, 0, st>>>(A, lda, M, K, 2 * Kp2, Kp2, Ap, nullptr, 0, 0);
+    const int64_t tb = Kp2 * Np;
+    pack_b_kernel<T, int32_t, false, true, 128, 2><<<(unsigned)std::min<int64_t>(ceil_div(tb, 256), 65535), 256, 0,
+                                                     st>>>(B, ldb, K, N, Np, Kp2, Bp, nullptr, 0, 0);
+    BTAS_CUDA_CHECK_LAUNCH();
+    GemmArgs g{};
+    g.Ap = Ap;
+    g.Bp = Bp;
+    g.Kp2 = Kp2;
+    g.M = M;
+    g.N = N;
+    g.mblocks = (int)(Mp / 128);
+    g.nblocks = (int)(Np / 128);
+    g.C = idx;
+    g.ldc = ldi;
+    g.Cprev = Cref;
+    g.ldcp = ldcr;
+    g.arg_row0 = row0;
+    return launch_gemm_epi<PK, true, kEpiCmp>(g, st);
+  }
   using G = GemmGeometry<T>;
   using P = MixArg<T>;
   static_assert(P::GM * 32 == G::BM, "argmin tiles use the 32/64-bit packed geometry");
@@ -526,7 +563,7 @@ BTAS_GEMM_HALF_DECL(double, gemm_f64_max);
 size_t gemm_ws_total(int dtype, int64_t M, int64_t N, int64_t K);
 #define BTAS_ARGMIN_DECL(T, NAME)                                                                                \
   int NAME(const T* A, int64_t lda, const T* B, int64_t ldb, const T* Cref, int64_t ldcr, int64_t M, int64_t N,    \
-           int64_t K, int64_t row0, int32_t* idx, int64_t ldi, unsigned char* ws, cudaStream_t st)
+           int64_t K, int64_t row0, int32_t* idx, int64_t ldi, bool keys, unsigned char* ws, cudaStream_t st)
 BTAS_ARGMIN_DECL(float, argmin_f32);
 BTAS_ARGMIN_DECL(int32_t, argmin_i32);
 BTAS_ARGMIN_DECL(double, argmin_f64);

@@ -21,7 +21,7 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.parametrize("dtype", DTYPES)
 def test_predecessors_match_oracle(cuda, dtype):
     for n, p, wr, seed in ((1, 0.5, (1, 9), 1), (2, 1.0, (1, 9), 2), (37, 0.3, (0, 5), 3), (130, 0.1, (1, 100), 4),
-                           (300, 0.5, (1, 3), 5), (257, 0.02, (0, 20), 6)):
+                           (300, 0.5, (1, 3), 5), (257, 0.02, (0, 20), 6), (90, 0.3, (1000, 20000), 7)):
         adj = random_graph_matrix(n, p, wr, seed, dtype=dtype)
         rep = bt.floyd_warshall(adj)
         pred = bt.predecessors(adj, rep)
@@ -72,3 +72,27 @@ def test_predecessors_at_scale(cuda):
         w = sum(int(a[u, v]) for u, v in zip(path, path[1:]))
         assert w == int(d[i, j])
     assert int((pred < 0).sum()) == n  # only the diagonal: the graph is strongly connected
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_argmin_key_path_equals_compare_path(cuda, dtype):
+    """btas_gemm_argmin's packed (value << 16 | k) key kernel (small integer
+    operands) and its compare-and-select kernel (operand bound unknown)
+    produce the same first-argmin indices."""
+    from paper_1701_04733_b200 import _lib
+    from paper_1701_04733_b200.matrix import _dtype_code, _workspace
+
+    n = 700
+    adj = random_graph_matrix(n, 0.4, (0, 50), 8, dtype=dtype)
+    d = bt.floyd_warshall(adj).distances.dist.data
+    b = adj.data.clone()
+    b.diagonal().fill_(_lib.I32_INF if dtype == torch.int32 else math.inf)
+    code = _dtype_code(dtype)
+    ws = _workspace.get(d.device, _lib.load().btas_gemm_workspace_bytes(code, n, n, n))
+    out = []
+    for bound in (4000.0, -1.0):
+        idx = torch.empty((n, n), dtype=torch.int32, device=d.device)
+        _lib.call("btas_gemm_argmin", code, 1, bound, d.data_ptr(), n, b.data_ptr(), n, d.data_ptr(), n, n, n, n, 0,
+                  idx.data_ptr(), n, ws.data_ptr(), ws.numel(), torch.cuda.current_stream().cuda_stream)
+        out.append(idx)
+    assert torch.equal(out[0], out[1])
