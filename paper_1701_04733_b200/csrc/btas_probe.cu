@@ -1,7 +1,7 @@
 // btas_probe_ceiling: the live roofline denominator for the tropical GEMM.
 // Runs the GEMM inner loop without global traffic — an 8x8 register
 // microtile, A operands in registers, B operands streamed from shared memory
-// with LDS.128 — for the instruction mix of each kernel path, one 256-thread
+// with LDS.128 — for the instruction mix of each kernel path, one 512-thread
 // CTA per SM, and reports candidate pairs per SM clock plus the SM clock the
 // run saw (from clock64 vs. event time).  tools/pipe_microbench.cu is the
 // standalone, wider version of the same measurement.
@@ -97,8 +97,13 @@ done:
   return rc;
 }
 
+// 16 warps per SM: enough latency hiding that the issue / pipe limit of the
+// mix, not the dependency chains, sets the figure (8 warps read 3 % low for
+// FADD2+FMNMX3: the GEMM kernel itself exceeded that ceiling)
+constexpr int kProbeThreads = 512;
+
 template <int MIX>
-__global__ void __launch_bounds__(256) probe_kernel(const uint32_t* __restrict__ gin, uint32_t* gout,
+__global__ void __launch_bounds__(kProbeThreads, 1) probe_kernel(const uint32_t* __restrict__ gin, uint32_t* gout,
                                                     long long* cycles) {
   __shared__ __align__(16) uint32_t sm[2048];
   for (int i = threadIdx.x; i < 2048; i += blockDim.x) sm[i] = gin[i];
@@ -152,14 +157,15 @@ int run_probe(double* ppc, double* mhz, double* tps) {
   std::vector<uint32_t> h(2048);
   std::vector<long long> hc(nsm);
   for (int i = 0; i < 2048; ++i) h[i] = MIX == 0 ? 0x3f800000u + (uint32_t)(i * 2654435761u % 100000u) : (uint32_t)(i % 97);
-  if (cudaMalloc(&din, 2048 * 4) || cudaMalloc(&dout, (size_t)nsm * 256 * 4) || cudaMalloc(&dcyc, nsm * 8)) goto done;
+  if (cudaMalloc(&din, 2048 * 4) || cudaMalloc(&dout, (size_t)nsm * kProbeThreads * 4) || cudaMalloc(&dcyc, nsm * 8))
+    goto done;
   if (cudaMemcpy(din, h.data(), 2048 * 4, cudaMemcpyHostToDevice)) goto done;
-  probe_kernel<MIX><<<nsm, 256>>>(din, dout, dcyc);  // warm-up
+  probe_kernel<MIX><<<nsm, kProbeThreads>>>(din, dout, dcyc);  // warm-up
   if (cudaDeviceSynchronize()) goto done;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  probe_kernel<MIX><<<nsm, 256>>>(din, dout, dcyc);
+  probe_kernel<MIX><<<nsm, kProbeThreads>>>(din, dout, dcyc);
   cudaEventRecord(e1);
   if (cudaEventSynchronize(e1)) goto done;
   {
@@ -167,7 +173,7 @@ int run_probe(double* ppc, double* mhz, double* tps) {
     cudaEventElapsedTime(&ms, e0, e1);
     if (cudaMemcpy(hc.data(), dcyc, nsm * 8, cudaMemcpyDeviceToHost)) goto done;
     const long long mx = *std::max_element(hc.begin(), hc.end());
-    const double pairs = 128.0 * (MIX == 2 ? 2.0 : 1.0) * kProbeIters * 256.0 * nsm;
+    const double pairs = 128.0 * (MIX == 2 ? 2.0 : 1.0) * kProbeIters * (double)kProbeThreads * nsm;
     *ppc = pairs / nsm / (double)mx;
     *mhz = (double)mx / (ms * 1e-3) / 1e6;
     *tps = pairs / (ms * 1e-3) / 1e12;
