@@ -1246,9 +1246,9 @@ def paths_arm(args, rank, world, dev):
                       "unreachable_pairs": unreachable},
            "roofline": {"bound": "alu", "achieved": round(ach, 3), "peak": round(peak, 3), "unit": "Tpair/s",
                         "frac": round(ach / peak, 4), "traffic": None,
-                        "work": "n^3 candidates (add, compare, two selects each)",
-                        "peak_source": "btas_probe_ceiling(i32 VIADDMNMX, 1 instruction per pair) x SMs x clock; "
-                                       "the argmin needs ~4 ALU ops per candidate"},
+                        "work": "n^3 candidates; small integer data: packed (value << 16 | k) keys, one "
+                                "VIADDMNMX per candidate (else compare-and-select, ~3 ALU ops)",
+                        "peak_source": "btas_probe_ceiling(i32 VIADDMNMX, 1 instruction per pair) x SMs x clock"},
            "clocks": clk, "gpu_launches": steps * 3}
     if rank == 0:
         print(json.dumps(res), flush=True)
