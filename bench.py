@@ -901,6 +901,21 @@ def apsp_cpu_baseline(workload, n):
             kind, what = "port", "NumPy restatement of apsp_by_squaring"
         return {"value": round(secs, 4), "unit": "s", "cores": cores, "kind": kind,
                 "sample": f"the full n={n} instance, {what}"}, ref
+    if workload == "fw" and btas is not None:
+        # the stock reference's floyd_warshall (apsp.py:93-133: numpy rounds,
+        # single-threaded like the reference) on a bounded instance, scaled by
+        # its n^3 work
+        m = 1024
+        sym = np.concatenate([blk for _, blk in dense_rows(m, 0.5, (1, 100), instance_seed(1, m))])
+        A = btas.TropicalMatrix(btas.SemiringKind.MIN_PLUS, sym)
+        btas.floyd_warshall(btas.TropicalMatrix(btas.SemiringKind.MIN_PLUS, sym[:64, :64]))  # warm-up
+        t = time.perf_counter()
+        btas.floyd_warshall(A)
+        secs = time.perf_counter() - t
+        return {"value": round(secs * (n / m) ** 3, 1), "unit": "s", "cores": 1, "kind": "reference",
+                "extrapolated": True,
+                "sample": f"stock btas.floyd_warshall on the n={m} instance ({secs:.2f} s, numpy rounds on one "
+                          f"core as the reference runs them), x (n/{m})^3"}, None
     sub = min(n, 4096)
     rows = [blk for r0, blk in dense_rows(n, 0.5, (1, 100), instance_seed(1, n), chunk_rows=1024) if r0 < sub]
     d = np.ascontiguousarray(np.concatenate(rows)[:sub, :sub])
