@@ -68,6 +68,8 @@ def parse(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the byte comparisons against the reference/oracle")
     ap.add_argument("--no-apsp", action="store_true", help="skip the APSP C4 measurement of the default run")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the C1 / C3 / C5 measurements of the default run")
     ap.add_argument("--apsp-n", type=int, default=65536, help="APSP C4 size inside the default run")
     return ap.parse_args(argv)
 
@@ -270,16 +272,15 @@ def main(argv=None):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    if args.workload in ("fw", "apsp"):
-        return apsp_arm(args, rank, world, dev)
-    if args.workload in ("matvec", "ewadd"):
-        return hbm_arm(args, rank, world, dev)
-    if args.workload == "graph":
-        return graph_arm(args, rank, world, dev)
-    if args.workload == "verify":
-        return verify_arm(args, rank, world, dev)
-    if args.workload == "paths":
-        return paths_arm(args, rank, world, dev)
+    arm = {"fw": apsp_arm, "apsp": apsp_arm, "matvec": hbm_arm, "ewadd": hbm_arm, "graph": graph_arm,
+           "verify": verify_arm, "paths": paths_arm}.get(args.workload)
+    if arm is not None:
+        res = arm(args, rank, world, dev)
+        if rank == 0:
+            print(json.dumps(res), flush=True)
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
 
     import paper_1701_04733_b200 as bt
     from paper_1701_04733_b200 import _lib
@@ -432,13 +433,19 @@ def main(argv=None):
     if "cpu_baseline" in result:
         result["_ref_gpairs"] = result["cpu_baseline"]["value"]
 
-    # ------------------------------------------------------------- APSP C4 (north-star scaling row)
-    if not args.no_apsp and args.workload == "gemm":
+    # ------------------------------------------------------------- the other BASELINE configs + C4
+    # Every config of BASELINE.json is measured inside the default run, each
+    # as a sub-line with its own roofline, clocks, e2e, cpu_baseline and
+    # parity: C1 (n=512 squaring), C3 (n=32768 FW), C5 (n=65536 max-plus
+    # matvec with 1 and 8 vectors, elementwise ⊕) and C4 (n=65536 squaring,
+    # row-sharded over the ranks under torchrun).  A watchdog keeps the GEMM
+    # line if anything stalls.
+    if args.workload == "gemm" and not (args.no_apsp and args.no_configs):
         del x, y, out, xs, ys
         torch.cuda.empty_cache()
 
         def give_up():  # a stuck exchange must not cost the GEMM line
-            result["apsp_c4"] = {"error": f"timed out after {APSP_WATCHDOG_S} s"}
+            result.setdefault("apsp_c4", {"error": f"timed out after {APSP_WATCHDOG_S} s"})
             result.pop("_ref_gpairs", None)
             if rank == 0:
                 print(json.dumps(result), flush=True)
@@ -448,9 +455,25 @@ def main(argv=None):
         timer.daemon = True
         timer.start()
         try:
-            result["apsp_c4"] = apsp_c4(args, rank, world, dev, result.get("_ref_gpairs"))
-        except Exception as exc:  # report, keep the GEMM line
-            result["apsp_c4"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+            if not args.no_configs:
+                result["configs"] = {}
+                subs = (("c1_apsp_n512", apsp_arm, dict(workload="apsp", n=512)),
+                        ("c3_fw_n32768", apsp_arm, dict(workload="fw", n=32768, steps=3)),
+                        ("c5_matvec_n65536_b1", hbm_arm, dict(workload="matvec", n=65536, batch=1)),
+                        ("c5_matvec_n65536_b8", hbm_arm, dict(workload="matvec", n=65536, batch=8)),
+                        # e2e of the 34 GB elementwise pair is PCIe-bound for seconds: its own arm has it
+                        ("c5_ewadd_n65536", hbm_arm, dict(workload="ewadd", n=65536, no_e2e=True)))
+                for key, arm, kw in subs:
+                    try:
+                        result["configs"][key] = arm(sub_args(args, **kw), rank, world, dev)
+                    except Exception as exc:  # report, keep the rest
+                        result["configs"][key] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+                    torch.cuda.empty_cache()
+            if not args.no_apsp:
+                try:
+                    result["apsp_c4"] = apsp_c4(args, rank, world, dev, result.get("_ref_gpairs"))
+                except Exception as exc:  # report, keep the GEMM line
+                    result["apsp_c4"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
         finally:
             timer.cancel()
     result.pop("_ref_gpairs", None)
@@ -461,7 +484,16 @@ def main(argv=None):
     return 0
 
 
-APSP_WATCHDOG_S = 900
+APSP_WATCHDOG_S = 1500
+
+
+def sub_args(args, **kw):
+    """A copy of the command-line namespace for one sub-measurement."""
+    ns = argparse.Namespace(**vars(args))
+    ns.steps = kw.pop("steps", args.steps)
+    for k, v in kw.items():
+        setattr(ns, k, v)
+    return ns
 
 
 def _max_over_ranks(v: float, world: int, dev) -> float:
@@ -861,9 +893,7 @@ def apsp_arm(args, rank, world, dev):
             rng = np.random.default_rng(0xC3)
             sample = sorted({0, n - 1, *rng.choice(n, 14, replace=False).tolist()})
             res["parity"] = _checks().closure_rows_parity(adj.data, d, sample, gen=(n, 0.5, (1, 100), seed))
-    if rank == 0:
-        print(json.dumps(res), flush=True)
-    return 0
+    return res
 
 
 def apsp_cpu_baseline(workload, n):
@@ -1047,9 +1077,7 @@ def hbm_arm(args, rank, world, dev):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         res["cpu_baseline"] = hbm_cpu_baseline(args.workload, a_sym, v_sym if args.workload == "matvec" else b_sym,
                                                nbytes, n)
-    if rank == 0:
-        print(json.dumps(res), flush=True)
-    return 0
+    return res
 
 
 def hbm_cpu_baseline(workload, a_sym, other_sym, nbytes, n):
@@ -1149,9 +1177,7 @@ def graph_arm(args, rank, world, dev):
                                "kind": "port", "extrapolated": True,
                                "sample": f"first {rows} rows of the instance via dense_rows "
                                "(numpy PCG64 + scatter), extrapolated to n rows"}
-    if rank == 0:
-        print(json.dumps(res), flush=True)
-    return 0
+    return res
 
 
 def verify_arm(args, rank, world, dev):
@@ -1217,9 +1243,7 @@ def verify_arm(args, rank, world, dev):
                                    "cores": len(os.sched_getaffinity(0)), "kind": "reference", "extrapolated": True,
                                    "sample": f"stock btas.find_apsp_violation on the n={m} instance ({secs:.2f} s), "
                                              f"x (n/{m})^3"}
-    if rank == 0:
-        print(json.dumps(res), flush=True)
-    return 0
+    return res
 
 
 def paths_arm(args, rank, world, dev):
@@ -1265,9 +1289,7 @@ def paths_arm(args, rank, world, dev):
                                 "VIADDMNMX per candidate (else compare-and-select, ~3 ALU ops)",
                         "peak_source": "btas_probe_ceiling(i32 VIADDMNMX, 1 instruction per pair) x SMs x clock"},
            "clocks": clk, "gpu_launches": steps * 3}
-    if rank == 0:
-        print(json.dumps(res), flush=True)
-    return 0
+    return res
 
 
 def reference_arm(args, rank, world):
