@@ -406,6 +406,13 @@ def main(argv=None):
     if not args.no_variants and args.workload == "gemm" and world == 1:
         result["variants"] = variants(n, dev, rank, check=not args.no_parity)
 
+    # ------------------------------------------------------------- one product row-sharded over the ranks
+    if world > 1 and args.workload == "gemm":
+        try:
+            result["gemm_row_sharded"] = gemm_row_sharded(args, x, y, out, n, rank, world, dev)
+        except Exception as exc:  # report, keep the line
+            result["gemm_row_sharded"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
     # ------------------------------------------------------------- stock reference on a row block (rank 0)
     # cpu_baseline (N = 1) and parity: the same operands, the reference's
     # btas.matmul on the first rows, byte-compared with the GPU's rows.
@@ -517,6 +524,37 @@ def _s16_ceiling(dev, sm_mhz=None):
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
     mhz = sm_mhz or probe["sm_mhz"]
     return probe["pairs_per_clk_sm"] * nsm * mhz * 1e6 / 1e12, probe["pairs_per_clk_sm"], mhz
+
+
+def gemm_row_sharded(args, x, y, out, n, rank, world, dev):
+    """SURVEY §8(e) GEMM row: ONE n x n product split by output rows over the
+    ranks (matmul_distributed: B replicated, the all-gather fused into the
+    GEMM epilogue as peer stores), strong scaling; every rank ends with the
+    whole product, compared bytewise with its own single-GPU product."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1701_04733_b200.sharded import matmul_distributed
+
+    prod = matmul_distributed(x, y)  # warm-up (symmetric-memory rendezvous)
+    torch.cuda.synchronize()
+    dist.barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = max(1, min(args.steps, 5))
+    s.record()
+    for _ in range(steps):
+        prod = matmul_distributed(x, y)
+    e.record()
+    torch.cuda.synchronize()
+    ms = _max_over_ranks(s.elapsed_time(e) / steps, world, dev)
+    same = bool(torch.equal(prod.data, out))  # out: this rank's own full product of the timed run
+    ok = torch.tensor([1 if same else 0], dtype=torch.int32, device=dev)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    return {"metric": f"row-sharded tropical GEMM G(add,min)/s at n={n}", "value": round(float(n) ** 3 /
+            (ms * 1e-3) / 1e9, 1), "unit": UNIT, "n_gpus": world, "steps": steps, "ms_per_step": round(ms, 3),
+            "higher_is_better": True, "scaling": "strong",
+            "exchange": os.environ.get("BTAS_EXCHANGE", "auto"),
+            "parity": {"equal_to_single_gpu_product_on_every_rank": bool(int(ok.item()))}}
 
 
 def distance_checksum(d) -> int:
