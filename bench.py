@@ -409,7 +409,7 @@ def main(argv=None):
     # ------------------------------------------------------------- one product row-sharded over the ranks
     if world > 1 and args.workload == "gemm":
         try:
-            result["gemm_row_sharded"] = gemm_row_sharded(args, x, y, out, n, rank, world, dev)
+            result["gemm_row_sharded"] = gemm_row_sharded(args, n, dtype, real, world, dev)
         except Exception as exc:  # report, keep the line
             result["gemm_row_sharded"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
@@ -526,16 +526,21 @@ def _s16_ceiling(dev, sm_mhz=None):
     return probe["pairs_per_clk_sm"] * nsm * mhz * 1e6 / 1e12, probe["pairs_per_clk_sm"], mhz
 
 
-def gemm_row_sharded(args, x, y, out, n, rank, world, dev):
-    """SURVEY §8(e) GEMM row: ONE n x n product split by output rows over the
-    ranks (matmul_distributed: B replicated, the all-gather fused into the
-    GEMM epilogue as peer stores), strong scaling; every rank ends with the
-    whole product, compared bytewise with its own single-GPU product."""
+def gemm_row_sharded(args, n, dtype, real, world, dev):
+    """SURVEY §8(e) GEMM row: ONE n x n product (the same operands on every
+    rank) split by output rows over the ranks (matmul_distributed: B
+    replicated, the all-gather fused into the GEMM epilogue as peer stores),
+    strong scaling; every rank ends with the whole product, compared bytewise
+    with its own single-GPU product."""
     import torch
     import torch.distributed as dist
 
+    import paper_1701_04733_b200 as bt
     from paper_1701_04733_b200.sharded import matmul_distributed
 
+    x, _ = gemm_inputs(n, dtype, dev, 0xB2000001, real)
+    y, _ = gemm_inputs(n, dtype, dev, 0xB2000002, real)
+    out = bt.matmul(x, y).data
     prod = matmul_distributed(x, y)  # warm-up (symmetric-memory rendezvous)
     torch.cuda.synchronize()
     dist.barrier()
@@ -547,7 +552,7 @@ def gemm_row_sharded(args, x, y, out, n, rank, world, dev):
     e.record()
     torch.cuda.synchronize()
     ms = _max_over_ranks(s.elapsed_time(e) / steps, world, dev)
-    same = bool(torch.equal(prod.data, out))  # out: this rank's own full product of the timed run
+    same = bool(torch.equal(prod.data, out))  # this rank's own single-GPU product
     ok = torch.tensor([1 if same else 0], dtype=torch.int32, device=dev)
     dist.all_reduce(ok, op=dist.ReduceOp.MIN)
     return {"metric": f"row-sharded tropical GEMM G(add,min)/s at n={n}", "value": round(float(n) ** 3 /
