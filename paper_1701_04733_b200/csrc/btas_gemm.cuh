@@ -432,6 +432,10 @@ struct GemmShape {
 // Cprev under g.verify_mode, record the first violating index, no store).
 enum { kEpiPlain = 0, kEpiAcc = 1, kEpiCmp = 2, kEpiBoth = 3, kEpiPeers = 4, kEpiVerify = 8 };
 
+#ifndef BTAS_L2_HINTS
+#define BTAS_L2_HINTS 1
+#endif
+
 // verifier epilogue: one output entry against the reference value
 template <class Out>
 BTAS_D void verify_entry(const GemmArgs& g, Out v, Out ref, int64_t row, int64_t col, bool& bad_any) {
@@ -491,6 +495,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
     if (warp == 0 && lane == 0) {
+#if BTAS_L2_HINTS
+      const uint64_t polA = l2_policy_evict_last(), polB = l2_policy_evict_first();
+#endif
       uint32_t it = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         int mb, nb;
@@ -503,8 +510,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
           const int s = it % ST;
           if (it >= (uint32_t)ST) mbar_wait(&empty[s], ((it / ST) - 1) & 1);
           mbar_arrive_expect_tx(&full[s], (uint32_t)((S::A_ELEMS + S::B_ELEMS) * sizeof(E)));
+#if BTAS_L2_HINTS
+          // A panels are shared by every tile of the 8-row group across the
+          // consecutive waves; B panels of a wave are streamed
+          bulk_g2s_hint(sA + s * S::A_ELEMS, gA + (size_t)kb * S::A_ELEMS, S::A_ELEMS * sizeof(E), &full[s], polA);
+          bulk_g2s_hint(sB + s * S::B_ELEMS, gB + (size_t)kb * S::B_ELEMS, S::B_ELEMS * sizeof(E), &full[s], polB);
+#else
           bulk_g2s(sA + s * S::A_ELEMS, gA + (size_t)kb * S::A_ELEMS, S::A_ELEMS * sizeof(E), &full[s]);
           bulk_g2s(sB + s * S::B_ELEMS, gB + (size_t)kb * S::B_ELEMS, S::B_ELEMS * sizeof(E), &full[s]);
+#endif
         }
       }
     }
