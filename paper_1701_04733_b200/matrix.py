@@ -391,10 +391,12 @@ def _stats_bound(st: _lib.Stats) -> float:
 
 def _sum_bound(*bounds: "float | None") -> "float | None":
     """|a ⊗ b| <= |a| + |b| for finite entries: the bound of a product's
-    finite results (None when an operand's bound is unknown)."""
+    finite results (None when an operand's bound is unknown).  Widened by
+    2^-20 relative: a float32 / float64 sum is rounded once and may land just
+    above the exact |a| + |b|, and the bound must stay an upper bound."""
     if any(b is None for b in bounds):
         return None
-    return float(sum(bounds))
+    return float(sum(bounds)) * (1.0 + 2.0**-20)
 
 
 def _max_bound(*bounds: "float | None") -> "float | None":

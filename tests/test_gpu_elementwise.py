@@ -68,7 +68,7 @@ def test_matvec_bound_selects_screen_free_path(cuda, dtype):
     # bounds propagate through products and ⊕ (|a (x) b| <= |a| + |b|)
     b = bt.TropicalMatrix(MIN, rand_sym(rng, k, 64, -7, 9), dtype=dtype)
     c = bt.matmul(bt.TropicalMatrix(MIN, asym, dtype=dtype), b)
-    assert c.abs_bound == a.abs_bound + b.abs_bound
+    assert a.abs_bound + b.abs_bound <= c.abs_bound <= (a.abs_bound + b.abs_bound) * (1 + 2**-19)
     assert float(np.abs(np.where(np.isfinite(c.to_numpy()), c.to_numpy(), 0)).max()) <= c.abs_bound
     assert bt.ew_add(c, c).abs_bound == c.abs_bound and bt.identity_matrix(MIN, 3, dtype=dtype).abs_bound == 0.0
 
