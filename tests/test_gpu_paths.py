@@ -96,3 +96,38 @@ def test_argmin_key_path_equals_compare_path(cuda, dtype):
                   idx.data_ptr(), n, ws.data_ptr(), ws.numel(), torch.cuda.current_stream().cuda_stream)
         out.append(idx)
     assert torch.equal(out[0], out[1])
+
+
+def test_predecessors_edge_cases(cuda):
+    """n = 1, an edgeless graph, negative weights without a negative cycle,
+    argument errors."""
+    one = bt.TropicalMatrix(MIN, [[0]], dtype=torch.int32)
+    assert bt.predecessors(one).cpu().tolist() == [[-1]]
+    assert bt.shortest_path(bt.predecessors(one), 0, 0) == [0]
+    empty = bt.TropicalMatrix.filled(MIN, 5, 5, dtype=torch.float32)
+    p = bt.predecessors(empty)
+    assert bool((p == -1).all()) and bt.shortest_path(p, 0, 4) is None
+    neg = bt.TropicalMatrix(MIN, [[0, 4, math.inf], [math.inf, 0, -2], [1, math.inf, 0]], dtype=torch.float64)
+    rep = bt.floyd_warshall(neg)
+    assert not rep.negative_cycle
+    p = bt.predecessors(neg, rep)
+    assert bt.shortest_path(p, 0, 2) == [0, 1, 2] and bt.shortest_path(p, 2, 1) == [2, 0, 1]
+    with pytest.raises(TypeError):
+        bt.predecessors(neg, "not a report")
+    with pytest.raises(bt.DtypeMismatch):
+        bt.predecessors(bt.TropicalMatrix(MIN, [[0, 1], [1, 0]], dtype=torch.int32),
+                        bt.DistanceMatrix(2, bt.TropicalMatrix(MIN, [[0, 1], [1, 0]], dtype=torch.float32)))
+    with pytest.raises(IndexError):
+        bt.shortest_path(p, 0, 7)
+
+
+def test_verifier_mixed_dtypes_and_errors(cuda):
+    """A float32 result checked against an int32 adjacency compares in
+    float64; shape / kind errors as the reference raises them."""
+    adj = random_graph_matrix(60, 0.3, (1, 20), 3, dtype=torch.int32)
+    d32 = bt.TropicalMatrix(MIN, bt.floyd_warshall(adj).distances.dist.to_lists(), dtype=torch.float32)
+    assert bt.find_apsp_violation(adj, bt.DistanceMatrix(60, d32)) is None
+    with pytest.raises(bt.DimensionMismatch):
+        bt.find_apsp_violation(adj, bt.DistanceMatrix(2, bt.identity_matrix(MIN, 2)))
+    with pytest.raises(TypeError):
+        bt.find_apsp_violation([[0]], bt.DistanceMatrix(1, bt.identity_matrix(MIN, 1)))
