@@ -381,6 +381,88 @@ __global__ void __launch_bounds__(kFw2Threads, MODE == kChecked ? 1 : 2)
     atomicOr(&f.flags[BTAS_FLAG_SATURATED], 1);
 }
 
+// ------------------------------------------------------------------ phase 2, exact integers
+// For exact integer data without negative weights (every candidate an exact
+// integer, no negative cycle) the distances do not depend on how the
+// candidates are grouped, so the panels take the standard blocked-FW update
+// with the closed pivot tile T* that phase 1 left in D:
+//   row panel  P' = T* (x) P        column panel  C' = C (x) T*
+// (T* has a zero diagonal, so the old value is among the candidates) — one
+// min-plus product per 128 x 128 tile instead of b barrier-separated rounds,
+// and the FINAL panels are emitted as the phase-3 operands.  Any candidate is
+// the length of a real path and every candidate the sequential program uses
+// is still formed, so D is the same bytes.
+template <class T>
+struct FwP {
+  static constexpr int b = FwB<T>::b, RI = b / 16, RJ = b / 32;  // 512 threads, RI x RJ outputs each
+};
+constexpr int kFwPThreads = 512;
+
+template <class T>
+__global__ void __launch_bounds__(kFwPThreads, 1) fw_panel_kernel(T* __restrict__ D, T* __restrict__ Scol,
+                                                                  T* __restrict__ Srow, uint32_t* __restrict__ Scol16,
+                                                                  uint32_t* __restrict__ Srow16, FwArgs f) {
+  constexpr int b = FwP<T>::b, RI = FwP<T>::RI, RJ = FwP<T>::RJ;
+  const bool row_panel = blockIdx.y == 0;
+  const int blk = (int)blockIdx.x;
+  if (blk == (int)(f.k0 / b)) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* Ls = reinterpret_cast<T*>(smem_raw);  // left operand, transposed: Ls[m][i]
+  T* Rs = Ls + b * b;                      // right operand: Rs[m][x]
+  const T inf = Traits<T>::eps(true);
+  const int64_t r0 = row_panel ? f.k0 : (int64_t)blk * b;  // the tile's rows / columns in D
+  const int64_t c0 = row_panel ? (int64_t)blk * b : f.k0;
+  for (int e = threadIdx.x; e < b * b; e += kFwPThreads) {
+    const int i = e / b, j = e % b;
+    const T x = (r0 + i < f.n && c0 + j < f.n) ? D[(r0 + i - f.slab_r0) * f.ld + c0 + j] : inf;
+    const T t = (f.k0 + i < f.n && f.k0 + j < f.n) ? D[(f.k0 + i - f.slab_r0) * f.ld + f.k0 + j] : inf;
+    if (row_panel) {  // P' = T* (x) P: left T*[k][m], right P[m][x]
+      Ls[j * b + i] = t;
+      Rs[i * b + j] = x;
+    } else {  // C' = C (x) T*: left C[x][m], right T*[m][k]
+      Ls[j * b + i] = x;
+      Rs[i * b + j] = t;
+    }
+  }
+  __syncthreads();
+  const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
+  T acc[RI][RJ];
+#pragma unroll
+  for (int i = 0; i < RI; ++i)
+#pragma unroll
+    for (int j = 0; j < RJ; ++j) acc[i][j] = inf;
+  bool sat = false;
+#pragma unroll 4
+  for (int m = 0; m < b; ++m) {
+    T l[RI], r[RJ];
+#pragma unroll
+    for (int i = 0; i < RI; ++i) l[i] = Ls[m * b + ty * RI + i];  // broadcast within the warp
+#pragma unroll
+    for (int j = 0; j < RJ; ++j) r[j] = Rs[m * b + tx * RJ + j];
+#pragma unroll
+    for (int i = 0; i < RI; ++i)
+#pragma unroll
+      for (int j = 0; j < RJ; ++j) relax<T, kFast>(acc[i][j], l[i], r[j], f.int_mode, f.limit, sat);
+  }
+  __syncthreads();  // Ls becomes the emission history h[k][x]
+  T* h = Ls;
+#pragma unroll
+  for (int i = 0; i < RI; ++i)
+#pragma unroll
+    for (int j = 0; j < RJ; ++j) {
+      const int oi = ty * RI + i, oj = tx * RJ + j;  // output row / column inside the tile
+      const int64_t row = r0 + oi, col = c0 + oj;
+      if (row < f.n && col < f.n) D[(row - f.slab_r0) * f.ld + col] = acc[i][j];
+      // h[k][x]: k along the pivot block, x along the panel
+      if (row_panel) h[oi * b + oj] = acc[i][j];
+      else h[oj * b + oi] = acc[i][j];
+    }
+  __syncthreads();
+  const bool out16 = row_panel ? emit_history(h, c0, f.BNb, f, Srow, Srow16)
+                               : emit_history(h, r0 - f.slab_r0, f.BMa, f, Scol, Scol16);
+  if (__syncthreads_or(out16) && threadIdx.x == 0) rflag_or(f, &f.ctrl->s16_overflow[0]);
+}
+
 __global__ void fill_u32_kernel(uint32_t* p, int64_t n, uint32_t v) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = v;
@@ -456,7 +538,6 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
   const int nblk = (int)ceil_div(n, b);
   const bool int_mode = Traits<T>::dtype == BTAS_I32 || integer_mode;
   const double limit = Traits<T>::dtype == BTAS_I32 ? (double)kI32Limit : Traits<T>::int_limit;
-  (void)max_abs;
   constexpr bool CHECKED = MODE == kChecked;
   constexpr int kLook = G::look;
 
@@ -495,17 +576,26 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
 
   const size_t smem1 = 2 * (size_t)b * b * sizeof(T);
   const size_t smem2 = (size_t)b * b * sizeof(T);  // phase 2: the history array only
+  const size_t smemP = 2 * (size_t)b * b * sizeof(T);  // exact-integer panels: both operands
   static unsigned long long configured = 0;
   if (!configured_on_current_device(configured)) {
     if (cudaFuncSetAttribute(fw_phase1_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem1) != cudaSuccess ||
         cudaFuncSetAttribute(fw_phase2_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem2) != cudaSuccess) {
+                             (int)smem2) != cudaSuccess ||
+        cudaFuncSetAttribute(fw_panel_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemP) !=
+            cudaSuccess) {
       (void)cudaGetLastError();
       return BTAS_ERR_CUDA;
     }
     mark_configured(configured);
   }
+  // exact integers without negative weights: the panel products
+  // (fw_panel_kernel) replace the b sequential phase-2 rounds
+  const bool exact_panels =
+      MODE == kFast && !CHECKED &&
+      (Traits<T>::dtype == BTAS_I32 ||
+       (integer_mode && (Traits<T>::dtype == BTAS_F64 || 2.0 * (double)(n + 1) * max_abs < 16777216.0)));
 
   // base GEMM descriptors over the full D; per launch only the k range
   // (which half of the panels), the row/col window and the skip ranges change
@@ -623,8 +713,13 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
     f.koff = slot * b;
     f.group_start = slot == 0;
     fw_phase1_kernel<T, MODE><<<1, kFw1Threads, smem1, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
-    if (nblk > 1)
-      fw_phase2_kernel<T, MODE><<<dim3(nblk, 2), kFw2Threads, smem2, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
+    if (nblk > 1) {
+      if (exact_panels)
+        fw_panel_kernel<T><<<dim3(nblk, 2), kFwPThreads, smemP, st>>>(D, scol, srow, scol16, srow16, f);
+      else
+        fw_phase2_kernel<T, MODE><<<dim3(nblk, 2), kFw2Threads, smem2, st>>>(D, rsp, csp, scol, srow, scol16,
+                                                                            srow16, f);
+    }
     BTAS_CUDA_CHECK_LAUNCH();
     return BTAS_OK;
   };
