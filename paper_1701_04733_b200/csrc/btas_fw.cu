@@ -176,14 +176,14 @@ BTAS_D void store_block(T* __restrict__ D, const FwArgs& f, int64_t r0, int64_t 
 
 // packed phase-3 operands from a history array h[k][x] (k = pivot round,
 // x = row (A operand, Scol) or col (B operand, Srow) inside the block at rc0)
-template <class T>
+template <class T, int HS = FwB<T>::b>
 BTAS_D bool emit_history(const T* __restrict__ h, int64_t rc0, int BLK, const FwArgs& f, T* __restrict__ P,
                          uint32_t* __restrict__ P16) {
-  constexpr int b = FwB<T>::b;
+  constexpr int b = FwB<T>::b;  // HS: row stride of h (padded histories avoid bank conflicts)
   bool out16 = false;
   for (int e = threadIdx.x; e < (b / 2) * b; e += blockDim.x) {
     const int kp = e / b, x = e - kp * b;
-    const T v0 = h[(2 * kp) * b + x], v1 = h[(2 * kp + 1) * b + x];
+    const T v0 = h[(2 * kp) * HS + x], v1 = h[(2 * kp + 1) * HS + x];
     const int64_t idx = packed_index(rc0 + x, f.koff + 2 * kp, f.Kp2, BLK);
     rstore(f, P + idx, v0);
     rstore(f, P + idx + 1, v1);
@@ -193,8 +193,8 @@ BTAS_D bool emit_history(const T* __restrict__ h, int64_t rc0, int BLK, const Fw
     for (int e = threadIdx.x; e < (b / 4) * b; e += blockDim.x) {
       const int wp = e / b, x = e - wp * b;
       const int k = 4 * wp;
-      const uint32_t w0 = s16_lane(h[k * b + x]) | (s16_lane(h[(k + 1) * b + x]) << 16);
-      const uint32_t w1 = s16_lane(h[(k + 2) * b + x]) | (s16_lane(h[(k + 3) * b + x]) << 16);
+      const uint32_t w0 = s16_lane(h[k * HS + x]) | (s16_lane(h[(k + 1) * HS + x]) << 16);
+      const uint32_t w1 = s16_lane(h[(k + 2) * HS + x]) | (s16_lane(h[(k + 3) * HS + x]) << 16);
       const int64_t idx = packed_index(rc0 + x, f.koff / 2 + 2 * wp, f.Kp2w, 128);
       rstore(f, P16 + idx, w0);
       rstore(f, P16 + idx + 1, w1);
@@ -406,9 +406,10 @@ __global__ void __launch_bounds__(kFwPThreads, 1) fw_panel_kernel(T* __restrict_
   const bool row_panel = blockIdx.y == 0;
   const int blk = (int)blockIdx.x;
   if (blk == (int)(f.k0 / b)) return;
+  constexpr int S = b + 16 / (int)sizeof(T);  // padded row stride: transposed stores hit distinct banks
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Ls = reinterpret_cast<T*>(smem_raw);  // left operand, transposed: Ls[m][i]
-  T* Rs = Ls + b * b;                      // right operand: Rs[m][x]
+  T* Rs = Ls + b * S;                      // right operand: Rs[m][x]
   const T inf = Traits<T>::eps(true);
   const int64_t r0 = row_panel ? f.k0 : (int64_t)blk * b;  // the tile's rows / columns in D
   const int64_t c0 = row_panel ? (int64_t)blk * b : f.k0;
@@ -417,11 +418,11 @@ __global__ void __launch_bounds__(kFwPThreads, 1) fw_panel_kernel(T* __restrict_
     const T x = (r0 + i < f.n && c0 + j < f.n) ? D[(r0 + i - f.slab_r0) * f.ld + c0 + j] : inf;
     const T t = (f.k0 + i < f.n && f.k0 + j < f.n) ? D[(f.k0 + i - f.slab_r0) * f.ld + f.k0 + j] : inf;
     if (row_panel) {  // P' = T* (x) P: left T*[k][m], right P[m][x]
-      Ls[j * b + i] = t;
-      Rs[i * b + j] = x;
+      Ls[j * S + i] = t;
+      Rs[i * S + j] = x;
     } else {  // C' = C (x) T*: left C[x][m], right T*[m][k]
-      Ls[j * b + i] = x;
-      Rs[i * b + j] = t;
+      Ls[j * S + i] = x;
+      Rs[i * S + j] = t;
     }
   }
   __syncthreads();
@@ -436,9 +437,9 @@ __global__ void __launch_bounds__(kFwPThreads, 1) fw_panel_kernel(T* __restrict_
   for (int m = 0; m < b; ++m) {
     T l[RI], r[RJ];
 #pragma unroll
-    for (int i = 0; i < RI; ++i) l[i] = Ls[m * b + ty * RI + i];  // broadcast within the warp
+    for (int i = 0; i < RI; ++i) l[i] = Ls[m * S + ty * RI + i];  // broadcast within the warp
 #pragma unroll
-    for (int j = 0; j < RJ; ++j) r[j] = Rs[m * b + tx * RJ + j];
+    for (int j = 0; j < RJ; ++j) r[j] = Rs[m * S + tx * RJ + j];
 #pragma unroll
     for (int i = 0; i < RI; ++i)
 #pragma unroll
@@ -453,13 +454,13 @@ __global__ void __launch_bounds__(kFwPThreads, 1) fw_panel_kernel(T* __restrict_
       const int oi = ty * RI + i, oj = tx * RJ + j;  // output row / column inside the tile
       const int64_t row = r0 + oi, col = c0 + oj;
       if (row < f.n && col < f.n) D[(row - f.slab_r0) * f.ld + col] = acc[i][j];
-      // h[k][x]: k along the pivot block, x along the panel
-      if (row_panel) h[oi * b + oj] = acc[i][j];
-      else h[oj * b + oi] = acc[i][j];
+      // h[k][x] (row stride S): k along the pivot block, x along the panel
+      if (row_panel) h[oi * S + oj] = acc[i][j];
+      else h[oj * S + oi] = acc[i][j];
     }
   __syncthreads();
-  const bool out16 = row_panel ? emit_history(h, c0, f.BNb, f, Srow, Srow16)
-                               : emit_history(h, r0 - f.slab_r0, f.BMa, f, Scol, Scol16);
+  const bool out16 = row_panel ? emit_history<T, S>(h, c0, f.BNb, f, Srow, Srow16)
+                               : emit_history<T, S>(h, r0 - f.slab_r0, f.BMa, f, Scol, Scol16);
   if (__syncthreads_or(out16) && threadIdx.x == 0) rflag_or(f, &f.ctrl->s16_overflow[0]);
 }
 
@@ -576,7 +577,7 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
 
   const size_t smem1 = 2 * (size_t)b * b * sizeof(T);
   const size_t smem2 = (size_t)b * b * sizeof(T);  // phase 2: the history array only
-  const size_t smemP = 2 * (size_t)b * b * sizeof(T);  // exact-integer panels: both operands
+  const size_t smemP = 2 * (size_t)b * (b + 16 / sizeof(T)) * sizeof(T);  // exact-integer panels: both operands
   static unsigned long long configured = 0;
   if (!configured_on_current_device(configured)) {
     if (cudaFuncSetAttribute(fw_phase1_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
