@@ -413,16 +413,27 @@ __global__ void __launch_bounds__(kFwPThreads, 1) fw_panel_kernel(T* __restrict_
   const T inf = Traits<T>::eps(true);
   const int64_t r0 = row_panel ? f.k0 : (int64_t)blk * b;  // the tile's rows / columns in D
   const int64_t c0 = row_panel ? (int64_t)blk * b : f.k0;
-  for (int e = threadIdx.x; e < b * b; e += kFwPThreads) {
+  // loads: all of a thread's elements are fetched before any shared-memory
+  // store (a load-store loop serialised one memory latency per element)
+  constexpr int kPer = b * b / kFwPThreads;  // elements per thread per operand
+  T xv[kPer], tv[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int e = (int)threadIdx.x + u * kFwPThreads;
     const int i = e / b, j = e % b;
-    const T x = (r0 + i < f.n && c0 + j < f.n) ? D[(r0 + i - f.slab_r0) * f.ld + c0 + j] : inf;
-    const T t = (f.k0 + i < f.n && f.k0 + j < f.n) ? D[(f.k0 + i - f.slab_r0) * f.ld + f.k0 + j] : inf;
+    xv[u] = (r0 + i < f.n && c0 + j < f.n) ? D[(r0 + i - f.slab_r0) * f.ld + c0 + j] : inf;
+    tv[u] = (f.k0 + i < f.n && f.k0 + j < f.n) ? D[(f.k0 + i - f.slab_r0) * f.ld + f.k0 + j] : inf;
+  }
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int e = (int)threadIdx.x + u * kFwPThreads;
+    const int i = e / b, j = e % b;
     if (row_panel) {  // P' = T* (x) P: left T*[k][m], right P[m][x]
-      Ls[j * S + i] = t;
-      Rs[i * S + j] = x;
+      Ls[j * S + i] = tv[u];
+      Rs[i * S + j] = xv[u];
     } else {  // C' = C (x) T*: left C[x][m], right T*[m][k]
-      Ls[j * S + i] = x;
-      Rs[i * S + j] = t;
+      Ls[j * S + i] = xv[u];
+      Rs[i * S + j] = tv[u];
     }
   }
   __syncthreads();
