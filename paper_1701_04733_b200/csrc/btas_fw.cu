@@ -180,24 +180,31 @@ template <class T, int HS = FwB<T>::b>
 BTAS_D bool emit_history(const T* __restrict__ h, int64_t rc0, int BLK, const FwArgs& f, T* __restrict__ P,
                          uint32_t* __restrict__ P16) {
   constexpr int b = FwB<T>::b;  // HS: row stride of h (padded histories avoid bank conflicts)
+  // rc0 is a multiple of b and b divides the packing blocks, so the b
+  // rows/columns stay inside one packed block: packed_index(rc0 + x, koff +
+  // 2 kp, Kp2, BLK) = base + (kp * BLK + x) * 2 with the divisions done once
+  const int64_t blk = rc0 / BLK, roff = rc0 - blk * BLK;
+  T* Pb = P + ((blk * f.Kp2 + f.koff / 2) * BLK + roff) * 2;
   bool out16 = false;
   for (int e = threadIdx.x; e < (b / 2) * b; e += blockDim.x) {
     const int kp = e / b, x = e - kp * b;
     const T v0 = h[(2 * kp) * HS + x], v1 = h[(2 * kp + 1) * HS + x];
-    const int64_t idx = packed_index(rc0 + x, f.koff + 2 * kp, f.Kp2, BLK);
-    rstore(f, P + idx, v0);
-    rstore(f, P + idx + 1, v1);
+    const int64_t idx = ((int64_t)kp * BLK + x) * 2;
+    rstore(f, Pb + idx, v0);
+    rstore(f, Pb + idx + 1, v1);
     out16 |= !s16_ok(v0) || !s16_ok(v1);
   }
   if (f.emit_s16) {
+    const int64_t blk16 = rc0 / 128, roff16 = rc0 - blk16 * 128;
+    uint32_t* P16b = P16 + ((blk16 * f.Kp2w + f.koff / 4) * 128 + roff16) * 2;
     for (int e = threadIdx.x; e < (b / 4) * b; e += blockDim.x) {
       const int wp = e / b, x = e - wp * b;
       const int k = 4 * wp;
       const uint32_t w0 = s16_lane(h[k * HS + x]) | (s16_lane(h[(k + 1) * HS + x]) << 16);
       const uint32_t w1 = s16_lane(h[(k + 2) * HS + x]) | (s16_lane(h[(k + 3) * HS + x]) << 16);
-      const int64_t idx = packed_index(rc0 + x, f.koff / 2 + 2 * wp, f.Kp2w, 128);
-      rstore(f, P16 + idx, w0);
-      rstore(f, P16 + idx + 1, w1);
+      const int64_t idx = ((int64_t)wp * 128 + x) * 2;
+      rstore(f, P16b + idx, w0);
+      rstore(f, P16b + idx + 1, w1);
     }
   }
   return out16;
@@ -406,10 +413,13 @@ __global__ void __launch_bounds__(kFwPThreads, 1) fw_panel_kernel(T* __restrict_
   const bool row_panel = blockIdx.y == 0;
   const int blk = (int)blockIdx.x;
   if (blk == (int)(f.k0 / b)) return;
-  constexpr int S = b + 16 / (int)sizeof(T);  // padded row stride: transposed stores hit distinct banks
+  // Ls (the transposed left operand) has an odd row stride, so the
+  // transposed stores of a warp hit 32 distinct banks; its reads are warp
+  // broadcasts (scalar).  Rs and the history keep 16-byte aligned rows.
+  constexpr int LS = b + 1, S = b + 16 / (int)sizeof(T);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Ls = reinterpret_cast<T*>(smem_raw);  // left operand, transposed: Ls[m][i]
-  T* Rs = Ls + b * S;                      // right operand: Rs[m][x]
+  T* Rs = Ls + b * S;                      // right operand: Rs[m][x] (Ls occupies b * LS <= b * S)
   const T inf = Traits<T>::eps(true);
   const int64_t r0 = row_panel ? f.k0 : (int64_t)blk * b;  // the tile's rows / columns in D
   const int64_t c0 = row_panel ? (int64_t)blk * b : f.k0;
@@ -429,10 +439,10 @@ __global__ void __launch_bounds__(kFwPThreads, 1) fw_panel_kernel(T* __restrict_
     const int e = (int)threadIdx.x + u * kFwPThreads;
     const int i = e / b, j = e % b;
     if (row_panel) {  // P' = T* (x) P: left T*[k][m], right P[m][x]
-      Ls[j * S + i] = tv[u];
+      Ls[j * LS + i] = tv[u];
       Rs[i * S + j] = xv[u];
     } else {  // C' = C (x) T*: left C[x][m], right T*[m][k]
-      Ls[j * S + i] = xv[u];
+      Ls[j * LS + i] = xv[u];
       Rs[i * S + j] = tv[u];
     }
   }
@@ -448,7 +458,7 @@ __global__ void __launch_bounds__(kFwPThreads, 1) fw_panel_kernel(T* __restrict_
   for (int m = 0; m < b; ++m) {
     T l[RI], r[RJ];
 #pragma unroll
-    for (int i = 0; i < RI; ++i) l[i] = Ls[m * S + ty * RI + i];  // broadcast within the warp
+    for (int i = 0; i < RI; ++i) l[i] = Ls[m * LS + ty * RI + i];  // broadcast within the warp
 #pragma unroll
     for (int j = 0; j < RJ; ++j) r[j] = Rs[m * S + tx * RJ + j];
 #pragma unroll
