@@ -578,7 +578,9 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
     const uint32_t inf16 = (uint32_t)kS16Inf | ((uint32_t)kS16Inf << 16);
     fill_u32_kernel<<<1024, 256, 0, st>>>(scol16, (int64_t)((W.total - W.scol16) / 4), inf16);
   }
-  const bool emit_s16 = int_mode && !CHECKED;
+  // the s16x2 phase-3 kernel streams 32 word pairs per stage: b = 128 (4-byte
+  // storage) only
+  const bool emit_s16 = int_mode && !CHECKED && sizeof(T) == 4;
 
   FwArgs f{};
   f.n = n;
@@ -874,7 +876,9 @@ int fw_dist_group_typed(int integer_mode, int stage, T* D, int64_t ld, int64_t n
   const int nblk = (int)ceil_div(n, b);
   const bool int_mode = Traits<T>::dtype == BTAS_I32 || integer_mode;
   const double limit = Traits<T>::dtype == BTAS_I32 ? (double)kI32Limit : Traits<T>::int_limit;
-  const bool emit_s16 = int_mode && !CHECKED;
+  // the s16x2 phase-3 kernel streams 32 word pairs per stage: b = 128 (4-byte
+  // storage) only
+  const bool emit_s16 = int_mode && !CHECKED && sizeof(T) == 4;
   FwCtrl* ctrl = reinterpret_cast<FwCtrl*>(ws + W.ctrl);
   T* rsp = reinterpret_cast<T*>(ws + W.rsp);
   T* csp = reinterpret_cast<T*>(ws + W.csp);

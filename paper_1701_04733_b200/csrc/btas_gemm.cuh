@@ -202,8 +202,8 @@ struct MixS16 {
   using Acc = uint32_t;
   using Out = OutT;
   // GNv = 8: 128 x 256 tiles, 8 x 16 microtile (12 LDS.128 per 256 DPX ops
-  // instead of 8 per 128)
-  static constexpr int GM = 4, GN = GNv, KP = 16, STAGES = 4;
+  // instead of 8 per 128).  32 word pairs (128 k) per stage, 3 stages.
+  static constexpr int GM = 4, GN = GNv, KP = 32, STAGES = 3;
   static constexpr int path = BTAS_PATH_S16X2;
   static constexpr bool kChecked = false;
   static constexpr bool kArg = false;
@@ -764,6 +764,7 @@ int launch_gemm_epi(const GemmArgs& g, cudaStream_t stream) {
     }
     mark_configured(configured);
   }
+  if (g.Kp2 % P::KP != 0) return BTAS_ERR_INVALID;  // whole pipeline stages only
   const int ntiles = g.mblocks * g.nblocks;
   const int grid = ntiles < device_sm_count() ? ntiles : device_sm_count();
   if (grid <= 0) return BTAS_OK;

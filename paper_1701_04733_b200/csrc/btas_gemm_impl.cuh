@@ -20,7 +20,8 @@ int device_sm_count();
 namespace gemm_impl {
 namespace {  // internal linkage: one copy per dtype translation unit
 
-constexpr int kKP = 16;  // k pairs per pipeline stage (all policies)
+constexpr int kKP = 16;    // k pairs per pipeline stage (32/64-bit policies)
+constexpr int kKP16 = 32;  // word pairs per pipeline stage of the s16x2 policy
 
 struct Ctrl {
   int32_t path;
@@ -47,7 +48,7 @@ WsLayout ws_layout(int dtype, int64_t M, int64_t N, int64_t K) {
   const size_t es = dtype == BTAS_F64 ? 8 : 4;
   const int64_t BM = dtype == BTAS_F64 ? 64 : 128, BN = 128;
   const int64_t Kp = round_up(K, 2 * kKP);               // 32-bit/64-bit paths
-  const int64_t Kw = round_up(ceil_div(K, 2), 2 * kKP);  // s16 words
+  const int64_t Kw = round_up(ceil_div(K, 2), 2 * kKP16);  // s16 words
   const int64_t Mp = round_up(M, BM), Np = round_up(N, BN);
   const int64_t Mp16 = round_up(M, 128), Np16 = round_up(N, 256);
   const size_t a32 = (size_t)Mp * Kp * es, b32 = (size_t)Np * Kp * es;
@@ -425,7 +426,7 @@ int gemm_typed(int integer_mode, const T* A, int64_t lda, const T* B, int64_t ld
   const int bn16 = 32 * s16_gn();
   if (int_mode) {
     const int64_t Kv = ceil_div(K, 2);              // words
-    const int64_t Kp2 = round_up(Kv, 2 * kKP) / 2;  // word pairs
+    const int64_t Kp2 = round_up(Kv, 2 * kKP16) / 2;  // word pairs
     const int64_t Mp = round_up(M, 128), Np = round_up(N, bn16);
     uint32_t* Ap = reinterpret_cast<uint32_t*>(ws + L.packA);
     uint32_t* Bp = reinterpret_cast<uint32_t*>(ws + L.packB);
