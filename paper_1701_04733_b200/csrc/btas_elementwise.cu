@@ -608,12 +608,16 @@ int matvec_launch(int int_mode, const T* A, int64_t lda, int64_t M, int64_t K, c
                        ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(V)) & 15) == 0;
   for (int64_t b0 = 0; b0 < batch;) {
     const int64_t left = batch - b0;
-    const int nb = (int)std::min<int64_t>(wide_ok && left > 4 ? kWideNB : 4, left);
+    // 5-8 vectors always; 3-4 vectors too when the bound removed the screen
+    // (the screen-free wide kernel beats the narrow one there, 6.6 vs 6.2
+    // TB/s at 4 vectors; with the screen it does not, tools/matvec_ab.py)
+    const bool use_wide = sizeof(T) == 4 && wide_ok && (left > 4 || (!SCREEN && left > 2));
+    const int nb = (int)std::min<int64_t>(use_wide ? kWideNB : 4, left);
     const T* Vb = V + b0 * ldv;
     T* Ob = Out + b0 * ldo;
     b0 += nb;
     if constexpr (sizeof(T) == 4) {
-      if (nb > 4) {
+      if (use_wide) {
         CUtensorMap mapA, mapV;
         if (!wide_tensor_map(&mapA, Traits<T>::dtype == BTAS_F32, A, M, K, lda, kWideRows) ||
             !wide_tensor_map(&mapV, Traits<T>::dtype == BTAS_F32, Vb, nb, K, ldv, kWideNB))
