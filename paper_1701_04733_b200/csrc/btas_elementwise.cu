@@ -113,15 +113,25 @@ __global__ void ewadd_kernel(const T* __restrict__ a, const T* __restrict__ b, T
     const uint4* av = reinterpret_cast<const uint4*>(a);
     const uint4* bv = reinterpret_cast<const uint4*>(b);
     uint4* ov = reinterpret_cast<uint4*>(o);
-    for (int64_t i = tid; i < n / V; i += stride) {
-      uint4 x = av[i], y = bv[i], z;
+    auto op = [](uint4 x, uint4 y) {
+      uint4 z;
       const T* xs = reinterpret_cast<const T*>(&x);
       const T* ys = reinterpret_cast<const T*>(&y);
       T* zs = reinterpret_cast<T*>(&z);
 #pragma unroll
       for (int v = 0; v < V; ++v) zs[v] = MIN ? (ys[v] < xs[v] ? ys[v] : xs[v]) : (ys[v] > xs[v] ? ys[v] : xs[v]);
-      ov[i] = z;
+      return z;
+    };
+    // two independent vectors per operand in flight per trip, streamed
+    // (evict-first) — each byte is touched once
+    const int64_t nv = n / V;
+    int64_t i = tid;
+    for (; i + stride < nv; i += 2 * stride) {
+      const uint4 x0 = __ldcs(av + i), y0 = __ldcs(bv + i), x1 = __ldcs(av + i + stride), y1 = __ldcs(bv + i + stride);
+      __stcs(ov + i, op(x0, y0));
+      __stcs(ov + i + stride, op(x1, y1));
     }
+    for (; i < nv; i += stride) __stcs(ov + i, op(__ldcs(av + i), __ldcs(bv + i)));
   }
   for (int64_t i = body + tid; i < n; i += stride) {
     const T x = a[i], y = b[i];
