@@ -538,7 +538,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
     if (skipped(mb, nb)) continue;
 
     // epilogue operands: for interior tiles the Z / Cprev values are loaded
-    // BEFORE the k loop, so their latency hides behind the add-min work
+    // at the start of the LAST k-stage (peeled below), so their latency hides
+    // behind that stage's add-min work while the main loop runs without 64
+    // more live registers (K1, "epilogue operand")
     Out* C = static_cast<Out*>(g.C);
     const Out* Z = (EPI & kEpiAcc) ? static_cast<const Out*>(g.Z) : nullptr;
     const Out* Cp = (EPI & kEpiCmp) ? static_cast<const Out*>(g.Cprev) : nullptr;
@@ -550,14 +552,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
                           !(Z != nullptr && Cp != nullptr);
     const int64_t rb = (int64_t)mb * BM + ty * 2, cb = (int64_t)nb * BN + tx * 2;
     Out xi[GM][2][GN][2];
-    if (interior && X != nullptr) {
-#pragma unroll
-      for (int i = 0; i < GM; ++i)
-#pragma unroll
-        for (int r = 0; r < 2; ++r)
-#pragma unroll
-          for (int j = 0; j < GN; ++j) ld2(X + (rb + i * 32 + r) * ldx + cb + j * 32, xi[i][r][j]);
-    }
 
     Acc acc[GM][2][GN][2];
     int32_t aidx[P::kArg ? GM : 1][2][P::kArg ? GN : 1][2];  // argmin k (predecessor product only)
@@ -573,7 +567,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
             if constexpr (P::kArg) aidx[i][r][j][c] = -1;
           }
 
-    for (int kb = 0; kb < nkb; ++kb, ++it) {
+    auto k_stage = [&](int kb) {
       const int s = it % ST;
       mbar_wait(&full[s], (it / ST) & 1);
       const E* tA = sA + s * S::A_ELEMS + ty * 4;
@@ -602,7 +596,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      ++it;
+    };
+    for (int kb = 0; kb < nkb - 1; ++kb) k_stage(kb);
+    if (interior && X != nullptr) {
+#pragma unroll
+      for (int i = 0; i < GM; ++i)
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int j = 0; j < GN; ++j) ld2(X + (rb + i * 32 + r) * ldx + cb + j * 32, xi[i][r][j]);
     }
+    k_stage(nkb - 1);
 
     // ------------------------------ epilogue ------------------------------
     // Interior tiles (every tile but the last row/column of tiles): operands
@@ -764,7 +769,7 @@ int launch_gemm_epi(const GemmArgs& g, cudaStream_t stream) {
     }
     mark_configured(configured);
   }
-  if (g.Kp2 % P::KP != 0) return BTAS_ERR_INVALID;  // whole pipeline stages only
+  if (g.Kp2 < P::KP || g.Kp2 % P::KP != 0) return BTAS_ERR_INVALID;  // whole pipeline stages only
   const int ntiles = g.mblocks * g.nblocks;
   const int grid = ntiles < device_sm_count() ? ntiles : device_sm_count();
   if (grid <= 0) return BTAS_OK;
