@@ -311,3 +311,31 @@ def test_f64_integer_path_epilogues(cuda, monkeypatch):
     want, neg, mults, _ = ot.apsp_by_squaring(adj.to_numpy(), "f64", True)
     assert (got.multiplications_performed, got.negative_cycle) == (mults, neg)
     assert got.distances.dist.to_numpy().tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_split_fixpoint_compare(cuda, dtype):
+    """K >= 4096: the plain product kernel plus the separate changed-rows pass
+    (btas_gemm_impl.cuh changed_rows_kernel) must raise FLAG_CHANGED exactly
+    when some entry's bits differ from Cprev — vector rows (N % 4 == 0) and
+    scalar rows (odd N), a single differing entry in the last row, and an
+    aliased Cprev (fused compare kept)."""
+    g = torch.Generator(device=cuda)
+    g.manual_seed(21)
+    for m, n, k in ((130, 256, 4096), (67, 129, 4100)):
+        a = torch.randint(1, 100, (m, k), generator=g, device=cuda).to(dtype)
+        b = torch.randint(1, 100, (k, n), generator=g, device=cuda).to(dtype)
+        want, f0 = bm._gemm(a, b, MIN, True)
+        assert int(f0[_lib.FLAG_CHANGED]) == 0
+        out = torch.empty_like(want)
+        _, f = bm._gemm(a, b, MIN, True, out=out, cprev=want.clone())
+        assert int(f[_lib.FLAG_CHANGED]) == 0 and torch.equal(out, want)
+        for r, c in ((m - 1, n - 1), (0, 0), (m // 2, 3)):
+            prev = want.clone()
+            prev[r, c] += 1
+            _, f = bm._gemm(a, b, MIN, True, out=out, cprev=prev)
+            assert int(f[_lib.FLAG_CHANGED]) == 1, (m, n, r, c)
+        # Cprev aliasing C: the fused compare (reads before it writes) stays
+        same = want.clone()
+        _, f = bm._gemm(a, b, MIN, True, out=same, cprev=same)
+        assert int(f[_lib.FLAG_CHANGED]) == 0 and torch.equal(same, want)

@@ -3,7 +3,7 @@ short K, accumulate in place) against the plain product, kernel time by CUDA
 events: how much of the bulk pass's gap to the C2 kernel is per-tile
 overhead (short K) and how much the accumulate epilogue.
 
-usage: python tools/gemm_k_sweep.py [n] [K,K,...] [reps]"""
+usage: python tools/gemm_k_sweep.py [n] [K,K,...] [reps] [plain,acc,cmp]"""
 import sys
 from pathlib import Path
 
@@ -17,6 +17,7 @@ from paper_1701_04733_b200.matrix import _gemm  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
 ks = [int(v) for v in (sys.argv[2] if len(sys.argv) > 2 else "1024,2048,4096").split(",")]
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+modes = (sys.argv[4] if len(sys.argv) > 4 else "plain,acc").split(",")
 dev = torch.device("cuda", 0)
 g = torch.Generator(device=dev)
 g.manual_seed(3)
@@ -27,14 +28,15 @@ c = torch.randint(0, 2000, (n, n), generator=g, device=dev, dtype=torch.int32)
 for K in ks:
     a = torch.randint(1, 100, (n, K), generator=g, device=dev, dtype=torch.int32)
     b = torch.randint(1, 100, (K, n), generator=g, device=dev, dtype=torch.int32)
-    for mode in ("plain", "acc"):
+    for mode in modes:
         out = c.clone() if mode == "acc" else torch.empty_like(c)
         z = out if mode == "acc" else None
-        _gemm(a, b, MIN, True, out=out, z=z)
+        cp = c if mode == "cmp" else None
+        _gemm(a, b, MIN, True, out=out, z=z, cprev=cp)
         torch.cuda.synchronize()
         _lib.gemm_timing(True)
         for _ in range(reps):
-            _gemm(a, b, MIN, True, out=out, z=z)
+            _gemm(a, b, MIN, True, out=out, z=z, cprev=cp)
         torch.cuda.synchronize()
         kms, kc = _lib.gemm_timing_read()
         _lib.gemm_timing(False)
