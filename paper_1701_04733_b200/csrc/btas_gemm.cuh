@@ -26,6 +26,8 @@
 //    the fixpoint compare against Cprev (apsp.py:161) and the diag<0 test.
 #pragma once
 
+#include <type_traits>
+
 #include "btas_common.cuh"
 
 namespace btas {
@@ -432,6 +434,13 @@ struct GemmShape {
 // Cprev under g.verify_mode, record the first violating index, no store).
 enum { kEpiPlain = 0, kEpiAcc = 1, kEpiCmp = 2, kEpiBoth = 3, kEpiPeers = 4, kEpiVerify = 8 };
 
+#ifndef BTAS_KP_UNROLL_PLAIN
+#define BTAS_KP_UNROLL_PLAIN 2
+#endif
+#ifndef BTAS_KP_UNROLL_EPI
+#define BTAS_KP_UNROLL_EPI 4
+#endif
+
 #ifndef BTAS_L2_HINTS
 #define BTAS_L2_HINTS 1
 #endif
@@ -567,12 +576,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tropical_gemm_kernel(const __
             if constexpr (P::kArg) aidx[i][r][j][c] = -1;
           }
 
+    // k-pair unroll of the inner loop (the register schedule ptxas picks
+    // differs per epilogue): 4 for the 32-bit integer mixes with an epilogue
+    // operand (accumulate K = 1024 0.912 -> 0.925, K = 8192 0.935 -> 0.947 of
+    // the ceiling; compare n = 65536 0.930 -> 0.954) and for MixI32 plain;
+    // 2 for the s16x2 plain product (4 measured 0.3 % slower) and for the
+    // float / 64-bit policies (they spill at 4).  profiles/r02_ab_unroll.txt
+    constexpr bool kNarrowInt = sizeof(Out) == 4 && std::is_integral_v<E> && !P::kChecked && !P::kArg;
+    constexpr int kKpUnroll = !kNarrowInt                                         ? 2
+                              : EPI != kEpiPlain                                   ? BTAS_KP_UNROLL_EPI
+                              : std::is_same_v<E, int32_t> ? 4  // MixI32: 0.987 -> 0.994
+                                                           : BTAS_KP_UNROLL_PLAIN;
     auto k_stage = [&](int kb) {
       const int s = it % ST;
       mbar_wait(&full[s], (it / ST) & 1);
       const E* tA = sA + s * S::A_ELEMS + ty * 4;
       const E* tB = sB + s * S::B_ELEMS + tx * 4;
-#pragma unroll 2
+#pragma unroll kKpUnroll
       for (int kp = 0; kp < KP; ++kp) {
         E a[GM][4], b[GN][4];
 #pragma unroll

@@ -333,53 +333,6 @@ __global__ void pack_b_kernel(const T* __restrict__ B, int64_t ldb, int64_t K, i
   }
 }
 
-// ------------------------------------------------------------------ split fixpoint compare
-// For long K the squaring step runs the PLAIN product kernel and compares C
-// with Cprev in this separate streaming pass: the compare epilogue's
-// instantiation schedules its main loop ~2.5 % slower than the plain one
-// (tools/gemm_k_sweep.py: n = 32768, K = 8192 plain 0.954 / cmp 0.925-0.930
-// of the ceiling), while this pass costs 2 * M * N * sizeof(T) bytes of HBM
-// (n = 65536 f32: 34 GB, ~5.5 ms against an 8.3 s product).  Same flag as
-// the fused epilogue: FLAG_CHANGED when any entry's bits differ.
-constexpr int64_t kSplitCmpMinK = 4096;
-
-template <class W>
-__global__ void __launch_bounds__(256) changed_rows_kernel(const W* __restrict__ C, int64_t ldc,
-                                                           const W* __restrict__ Cp, int64_t ldcp, int64_t M,
-                                                           int64_t N, int32_t* flags) {
-  constexpr int V = 16 / (int)sizeof(W);
-  const volatile int32_t* seen = flags + BTAS_FLAG_CHANGED;
-  const bool vec = ldc % V == 0 && ldcp % V == 0 && N % V == 0 && reinterpret_cast<uintptr_t>(C) % 16 == 0 &&
-                   reinterpret_cast<uintptr_t>(Cp) % 16 == 0;
-  bool diff = false;
-  for (int64_t r = blockIdx.x; r < M; r += gridDim.x) {
-    if (diff || *seen != 0) break;  // the answer is known: stop reading
-    const W* c = C + r * ldc;
-    const W* p = Cp + r * ldcp;
-    if (vec) {
-      const uint4* c4 = reinterpret_cast<const uint4*>(c);
-      const uint4* p4 = reinterpret_cast<const uint4*>(p);
-      const int64_t nv = N / V;
-#pragma unroll 4
-      for (int64_t e = threadIdx.x; e < nv; e += blockDim.x) {
-        const uint4 a = c4[e];
-        const uint4 b = __ldcs(p4 + e);
-        diff |= ((a.x ^ b.x) | (a.y ^ b.y) | (a.z ^ b.z) | (a.w ^ b.w)) != 0u;
-      }
-    } else {
-      for (int64_t e = threadIdx.x; e < N; e += blockDim.x) diff |= c[e] != p[e];
-    }
-  }
-  if (__syncthreads_or(diff) && threadIdx.x == 0) atomicOr(flags + BTAS_FLAG_CHANGED, 1);
-}
-
-template <class T>
-bool ranges_overlap(const T* a, int64_t lda, const T* b, int64_t ldb, int64_t M, int64_t N) {
-  const uintptr_t a0 = reinterpret_cast<uintptr_t>(a), a1 = reinterpret_cast<uintptr_t>(a + (M - 1) * lda + N);
-  const uintptr_t b0 = reinterpret_cast<uintptr_t>(b), b1 = reinterpret_cast<uintptr_t>(b + (M - 1) * ldb + N);
-  return a0 < b1 && b0 < a1;
-}
-
 // ------------------------------------------------------------------ driver
 template <class T, bool MIN>
 int gemm_typed(int integer_mode, const T* A, int64_t lda, const T* B, int64_t ldb, const T* Z, int64_t ldz, T* C,
@@ -409,8 +362,6 @@ int gemm_typed(int integer_mode, const T* A, int64_t lda, const T* B, int64_t ld
   BTAS_CUDA_CHECK_LAUNCH();
 
   const int fast = kIsF64 ? BTAS_PATH_FAST64 : BTAS_PATH_FAST32;
-  const bool split_cmp = Cprev != nullptr && Z == nullptr && n_peers == 0 && x.first_bad == nullptr &&
-                         K >= kSplitCmpMinK && !ranges_overlap(C, ldc, Cprev, ldcp, M, N);
   GemmArgs g{};  // 32/64-bit paths (FAST and CHECKED share the packing)
   {
     const int64_t Kp2 = round_up(K, 2 * kKP) / 2;
@@ -436,7 +387,7 @@ int gemm_typed(int integer_mode, const T* A, int64_t lda, const T* B, int64_t ld
     g.ldz = ldz;
     g.C = C;
     g.ldc = ldc;
-    g.Cprev = split_cmp ? nullptr : Cprev;
+    g.Cprev = Cprev;
     g.ldcp = ldcp;
     g.flags = flags;
     g.gate = &ctrl->path;
@@ -523,13 +474,6 @@ int gemm_typed(int integer_mode, const T* A, int64_t lda, const T* B, int64_t ld
     }
   }
   timing_end(st, t0);
-  if (split_cmp) {
-    using W = std::conditional_t<sizeof(T) == 8, unsigned long long, uint32_t>;
-    const unsigned grid = (unsigned)std::min<int64_t>(M, 4 * (int64_t)device_sm_count());
-    changed_rows_kernel<W><<<grid, 256, 0, st>>>(reinterpret_cast<const W*>(C), ldc,
-                                                 reinterpret_cast<const W*>(Cprev), ldcp, M, N, flags);
-    BTAS_CUDA_CHECK_LAUNCH();
-  }
   return BTAS_OK;
 }
 

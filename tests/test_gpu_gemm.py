@@ -314,12 +314,11 @@ def test_f64_integer_path_epilogues(cuda, monkeypatch):
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
-def test_split_fixpoint_compare(cuda, dtype):
-    """K >= 4096: the plain product kernel plus the separate changed-rows pass
-    (btas_gemm_impl.cuh changed_rows_kernel) must raise FLAG_CHANGED exactly
-    when some entry's bits differ from Cprev — vector rows (N % 4 == 0) and
-    scalar rows (odd N), a single differing entry in the last row, and an
-    aliased Cprev (fused compare kept)."""
+def test_fixpoint_compare_long_k(cuda, dtype):
+    """K >= 4096 (the unroll-4 compare epilogue of the 32-bit integer mixes):
+    FLAG_CHANGED exactly when some entry's bits differ from Cprev — even and
+    odd N, a single differing entry anywhere, and Cprev aliasing C (the
+    epilogue reads Cprev before it stores)."""
     g = torch.Generator(device=cuda)
     g.manual_seed(21)
     for m, n, k in ((130, 256, 4096), (67, 129, 4100)):
@@ -335,7 +334,7 @@ def test_split_fixpoint_compare(cuda, dtype):
             prev[r, c] += 1
             _, f = bm._gemm(a, b, MIN, True, out=out, cprev=prev)
             assert int(f[_lib.FLAG_CHANGED]) == 1, (m, n, r, c)
-        # Cprev aliasing C: the fused compare (reads before it writes) stays
+        # Cprev aliasing C
         same = want.clone()
         _, f = bm._gemm(a, b, MIN, True, out=same, cprev=same)
         assert int(f[_lib.FLAG_CHANGED]) == 0 and torch.equal(same, want)
