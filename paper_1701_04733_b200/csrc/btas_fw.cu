@@ -21,6 +21,7 @@
 // otherwise the 32-bit kernel; the masked variant (reference screen failed)
 // uses per-candidate overflow masking throughout.
 #include <algorithm>
+#include <type_traits>
 
 #include "btas_gemm.cuh"
 
@@ -485,6 +486,171 @@ __global__ void __launch_bounds__(kFwPThreads, 1) fw_panel_kernel(T* __restrict_
   if (__syncthreads_or(out16) && threadIdx.x == 0) rflag_or(f, &f.ctrl->s16_overflow[0]);
 }
 
+// Half-tile panels for 4-byte storage (b = 128): CTA (blk, half) computes
+// 64 output rows of one panel tile with 256 threads and 100 KB of shared
+// memory, so two CTAs share an SM and one CTA's operand loads and emission
+// overlap the other's add-min loop (the full-tile kernel above runs one
+// 135 KB CTA per SM: load, compute, emit in sequence).  Per k: the left
+// operand's 8 rows of a warp are two broadcast LDS.128, the right operand's
+// 4 columns of a lane are strided (x = lane + 32 j), so those reads, the D
+// stores and both history layouts are bank-conflict free.
+constexpr int kFwHThreads = 256;
+template <class T>
+struct FwH {
+  static constexpr int b = 128, HR = 64;         // pivot block, output rows per CTA
+  static constexpr int LS = HR + 4, RS = b + 4;  // 16-byte aligned row strides
+  static constexpr size_t smem = (size_t)(b * LS + b * RS) * sizeof(T);
+};
+
+// packed phase-3 operands from a partial history h[k - k_lo][x - x_lo]
+// (k in [k_lo, k_lo + KN), x in [x_lo, x_lo + XN)), as emit_history
+template <class T, int HS, int KN, int XN>
+BTAS_D bool emit_part(const T* __restrict__ h, int k_lo, int x_lo, int64_t rc0, int BLK, const FwArgs& f,
+                      T* __restrict__ P, uint32_t* __restrict__ P16) {
+  const int64_t blk = rc0 / BLK, roff = rc0 - blk * BLK;
+  T* Pb = P + ((blk * f.Kp2 + f.koff / 2) * BLK + roff) * 2;
+  bool out16 = false;
+  for (int e = threadIdx.x; e < (KN / 2) * XN; e += blockDim.x) {
+    const int kp = e / XN, xl = e - kp * XN;
+    const T v0 = h[(2 * kp) * HS + xl], v1 = h[(2 * kp + 1) * HS + xl];
+    const int64_t idx = ((int64_t)(k_lo / 2 + kp) * BLK + x_lo + xl) * 2;
+    rstore(f, Pb + idx, v0);
+    rstore(f, Pb + idx + 1, v1);
+    out16 |= !s16_ok(v0) || !s16_ok(v1);
+  }
+  if (f.emit_s16) {
+    const int64_t blk16 = rc0 / 128, roff16 = rc0 - blk16 * 128;
+    uint32_t* P16b = P16 + ((blk16 * f.Kp2w + f.koff / 4) * 128 + roff16) * 2;
+    for (int e = threadIdx.x; e < (KN / 4) * XN; e += blockDim.x) {
+      const int wp = e / XN, xl = e - wp * XN;
+      const int k = 4 * wp;
+      const uint32_t w0 = s16_lane(h[k * HS + xl]) | (s16_lane(h[(k + 1) * HS + xl]) << 16);
+      const uint32_t w1 = s16_lane(h[(k + 2) * HS + xl]) | (s16_lane(h[(k + 3) * HS + xl]) << 16);
+      const int64_t idx = ((int64_t)(k_lo / 4 + wp) * 128 + x_lo + xl) * 2;
+      rstore(f, P16b + idx, w0);
+      rstore(f, P16b + idx + 1, w1);
+    }
+  }
+  return out16;
+}
+
+template <class T>
+__global__ void __launch_bounds__(kFwHThreads, 2) fw_panel_half_kernel(T* __restrict__ D, T* __restrict__ Scol,
+                                                                       T* __restrict__ Srow,
+                                                                       uint32_t* __restrict__ Scol16,
+                                                                       uint32_t* __restrict__ Srow16, FwArgs f) {
+  static_assert(sizeof(T) == 4, "b = 128 storage");
+  constexpr int b = FwH<T>::b, HR = FwH<T>::HR, LS = FwH<T>::LS, RS = FwH<T>::RS;
+  const bool row_panel = blockIdx.y == 0;
+  const int blk = (int)(blockIdx.x >> 1), half = (int)(blockIdx.x & 1);
+  if (blk == (int)(f.k0 / b)) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* Ls = reinterpret_cast<T*>(smem_raw);  // Ls[m][i] = left[i][m]
+  T* Rs = Ls + b * LS;                     // Rs[m][x] = right[m][x]
+  const T inf = Traits<T>::eps(true);
+  const int w = (int)threadIdx.x >> 5, lane = (int)threadIdx.x & 31;
+  // the tile in D; row panel P' = T* (x) P, column panel C' = C (x) T*.
+  // left[i][m] = D[lr0 + i][k0 + m] (T* rows / C rows of this half),
+  // right[m][x] = D[k0 + m][rc0 + x] (P / T*)
+  const int64_t r0 = row_panel ? f.k0 : (int64_t)blk * b;
+  const int64_t c0 = row_panel ? (int64_t)blk * b : f.k0;
+  const int64_t lr0 = (row_panel ? f.k0 : r0) + half * HR;
+  const int64_t rc0 = row_panel ? c0 : f.k0;
+  auto at = [&](int64_t row, int64_t col) -> T {
+    return (row < f.n && col < f.n) ? D[(row - f.slab_r0) * f.ld + col] : inf;
+  };
+  {  // left operand: a warp reads 4 rows x 8 columns (four full 32-byte
+     // sectors) and stores them transposed into 32 distinct banks
+    constexpr int kQ = HR * b / 32 / (kFwHThreads / 32);  // patches per warp
+    T v[kQ];
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+      const int p = w + 8 * q;
+      const int i = 4 * (p & 15) + (lane & 3), m = 8 * (p >> 4) + (lane >> 2);
+      v[q] = at(lr0 + i, f.k0 + m);
+    }
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+      const int p = w + 8 * q;
+      const int i = 4 * (p & 15) + (lane & 3), m = 8 * (p >> 4) + (lane >> 2);
+      Ls[m * LS + i] = v[q];
+    }
+  }
+  {  // right operand: row-major, 4 consecutive columns per thread
+    constexpr int kQ = b * b / 4 / kFwHThreads;
+    const bool vec = (f.ld % 4) == 0 && (reinterpret_cast<uintptr_t>(D) % 16) == 0 && rc0 + b <= f.n;
+    uint4 v[kQ];
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+      const int e = (int)threadIdx.x + kFwHThreads * q;
+      const int m = e >> 5, x = 4 * (e & 31);
+      const int64_t row = f.k0 + m;
+      if (vec && row < f.n) {
+        v[q] = *reinterpret_cast<const uint4*>(D + (row - f.slab_r0) * f.ld + rc0 + x);
+      } else {
+        v[q].x = __builtin_bit_cast(uint32_t, at(row, rc0 + x));
+        v[q].y = __builtin_bit_cast(uint32_t, at(row, rc0 + x + 1));
+        v[q].z = __builtin_bit_cast(uint32_t, at(row, rc0 + x + 2));
+        v[q].w = __builtin_bit_cast(uint32_t, at(row, rc0 + x + 3));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+      const int e = (int)threadIdx.x + kFwHThreads * q;
+      const int m = e >> 5, x = 4 * (e & 31);
+      *reinterpret_cast<uint4*>(Rs + m * RS + x) = v[q];
+    }
+  }
+  __syncthreads();
+  T acc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = inf;
+  bool sat = false;
+#pragma unroll 4
+  for (int m = 0; m < b; ++m) {
+    T l[8], r[4];
+    lds4(Ls + m * LS + w * 8, l);  // broadcast within the warp
+    lds4(Ls + m * LS + w * 8 + 4, l + 4);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) r[j] = Rs[m * RS + lane + 32 * j];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) relax<T, kFast>(acc[i][j], l[i], r[j], f.int_mode, f.limit, sat);
+  }
+  __syncthreads();  // the operand buffers become the emission history
+  T* h = Ls;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int orow = half * HR + w * 8 + i;  // output row inside the tile
+    const int64_t row = r0 + orow;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int x = lane + 32 * j;
+      if (row < f.n && c0 + x < f.n) D[(row - f.slab_r0) * f.ld + c0 + x] = acc[i][j];
+      if (row_panel) h[(w * 8 + i) * RS + x] = acc[i][j];  // h[k - 64 half][x]
+    }
+  }
+  if (!row_panel) {  // h[k][x - 64 half] = C'[x][k]: 8 consecutive x per (thread, k)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      T* hp = h + (lane + 32 * j) * LS + w * 8;
+      *reinterpret_cast<uint4*>(hp) = make_uint4(
+          __builtin_bit_cast(uint32_t, acc[0][j]), __builtin_bit_cast(uint32_t, acc[1][j]),
+          __builtin_bit_cast(uint32_t, acc[2][j]), __builtin_bit_cast(uint32_t, acc[3][j]));
+      *reinterpret_cast<uint4*>(hp + 4) = make_uint4(
+          __builtin_bit_cast(uint32_t, acc[4][j]), __builtin_bit_cast(uint32_t, acc[5][j]),
+          __builtin_bit_cast(uint32_t, acc[6][j]), __builtin_bit_cast(uint32_t, acc[7][j]));
+    }
+  }
+  __syncthreads();
+  const bool out16 = row_panel ? emit_part<T, RS, HR, b>(h, half * HR, 0, c0, f.BNb, f, Srow, Srow16)
+                               : emit_part<T, LS, b, HR>(h, 0, half * HR, r0 - f.slab_r0, f.BMa, f, Scol, Scol16);
+  if (__syncthreads_or(out16) && threadIdx.x == 0) rflag_or(f, &f.ctrl->s16_overflow[0]);
+}
+
 __global__ void fill_u32_kernel(uint32_t* p, int64_t n, uint32_t v) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = v;
@@ -555,6 +721,7 @@ template <class T, int MODE>
 int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, double min_finite, int32_t* flags,
              unsigned char* ws, cudaStream_t st) {
   using G = FwGeom<T>;
+  using T4 = std::conditional_t<sizeof(T) == 4, T, float>;  // the half-tile panel kernel's storage
   const FwWs W = fw_ws<T>(n);
   const int b = G::b;
   const int nblk = (int)ceil_div(n, b);
@@ -608,7 +775,9 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
         cudaFuncSetAttribute(fw_phase2_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem2) != cudaSuccess ||
         cudaFuncSetAttribute(fw_panel_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemP) !=
-            cudaSuccess) {
+            cudaSuccess ||
+        (sizeof(T) == 4 && cudaFuncSetAttribute(fw_panel_half_kernel<T4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)FwH<T4>::smem) != cudaSuccess)) {
       (void)cudaGetLastError();
       return BTAS_ERR_CUDA;
     }
@@ -738,7 +907,10 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
     f.group_start = slot == 0;
     fw_phase1_kernel<T, MODE><<<1, kFw1Threads, smem1, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
     if (nblk > 1) {
-      if (exact_panels)
+      if (exact_panels && sizeof(T) == 4)
+        fw_panel_half_kernel<T4><<<dim3(2 * nblk, 2), kFwHThreads, FwH<T4>::smem, st>>>(
+            reinterpret_cast<T4*>(D), reinterpret_cast<T4*>(scol), reinterpret_cast<T4*>(srow), scol16, srow16, f);
+      else if (exact_panels)
         fw_panel_kernel<T><<<dim3(nblk, 2), kFwPThreads, smemP, st>>>(D, scol, srow, scol16, srow16, f);
       else
         fw_phase2_kernel<T, MODE><<<dim3(nblk, 2), kFw2Threads, smem2, st>>>(D, rsp, csp, scol, srow, scol16,
