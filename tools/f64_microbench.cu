@@ -51,6 +51,20 @@ __global__ void __launch_bounds__(256) kern(const double* __restrict__ gin, doub
           const double s0 = __dadd_rn(a[i][0], b[j][0]), s1 = __dadd_rn(a[i][1], b[j][1]);
           const bool p0 = s0 < c, p1 = s1 < c;
           c = __hiloint2double(p0 ? __double2hiint(s0) : __double2hiint(c), p1 ? __double2loint(s1) : __double2loint(c));
+        } else if (MODE == 8 || MODE == 9) {  // hybrid: part of the accumulators compare
+          // on the FP64 pipe (DSETP), the rest as signed int64 keys on the ALU
+          // pipe (exact for non-negative doubles and +-inf): 8 = half, 9 = 3/4 on the ALU
+          const double s0 = __dadd_rn(a[i][0], b[j][0]), s1 = __dadd_rn(a[i][1], b[j][1]);
+          const bool alu = MODE == 8 ? (j & 1) != 0 : (j & 3) != 0;
+          if (alu) {
+            long long k = __double_as_longlong(c), k0 = __double_as_longlong(s0), k1 = __double_as_longlong(s1);
+            k = k0 < k ? k0 : k;
+            k = k1 < k ? k1 : k;
+            c = __longlong_as_double(k);
+          } else {
+            c = s0 < c ? s0 : c;
+            c = s1 < c ? s1 : c;
+          }
         } else if (MODE == 5) {  // ternary compare (DSETP + 2 SEL)
           const double s0 = __dadd_rn(a[i][0], b[j][0]), s1 = __dadd_rn(a[i][1], b[j][1]);
           const double m = s1 < s0 ? s1 : s0;
@@ -105,7 +119,7 @@ void run(const char* name, int bps) {
 }
 
 int main() {
-  for (int bps = 1; bps <= 1; ++bps) {
+  for (int bps = 1; bps <= 2; ++bps) {
     run<0>("f64 DADD + fmin chain", bps);
     run<1>("f64 DADD + fmin tree", bps);
     run<2>("f64 DADD only (2 per pair)", bps);
@@ -114,6 +128,8 @@ int main() {
     run<5>("f64 DADD + ternary tree", bps);
     run<6>("f64 DADD + ternary chain", bps);
     run<7>("f64 DADD + DSETP + 1 SEL (cost probe)", bps);
+    run<8>("f64 DADD + hybrid 1/2 DSETP, 1/2 int64 key", bps);
+    run<9>("f64 DADD + hybrid 1/4 DSETP, 3/4 int64 key", bps);
   }
   return 0;
 }
