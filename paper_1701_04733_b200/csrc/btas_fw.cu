@@ -213,16 +213,28 @@ BTAS_D bool emit_history(const T* __restrict__ h, int64_t rc0, int BLK, const Fw
 
 // ------------------------------------------------------------------ phase 1
 // smem: rs[k][c] (pivot-row history), cT[k][a] (pivot-column history)
-// One CTA of 32 x 32 threads (R1 x R1 values each): the b sequential rounds
-// are barrier-latency-bound, so the pivot tile is spread over 32 warps.
-constexpr int kFw1Threads = 1024;
+// One CTA of 16 x 32 threads (RI x RJ = 8 x 4 values each, b = 128; 4 x 2
+// for b = 64): the b sequential rounds are barrier-latency-bound, so the
+// pivot tile is spread over 16 warps (32 warps of 4 x 4: 1-2 us slower per
+// pivot block, profiles/r02_ab_phase1_threads.txt).
+#ifndef BTAS_FW1_THREADS
+#define BTAS_FW1_THREADS 512
+#endif
+constexpr int kFw1Threads = BTAS_FW1_THREADS;
+
+template <class T>
+struct Fw1 {
+  static constexpr int b = FwB<T>::b, TY = kFw1Threads / 32, RI = b / TY, RJ = b / 32;
+  static constexpr int U = RI > RJ ? RI : RJ;  // rounds per unrolled step (both owners static)
+};
 
 template <class T, int MODE>
 __global__ void __launch_bounds__(kFw1Threads) fw_phase1_kernel(T* __restrict__ D, T* __restrict__ rowsnapP,
                                                                 T* __restrict__ colsnapT, T* __restrict__ Scol,
                                                                 T* __restrict__ Srow, uint32_t* __restrict__ Scol16,
                                                                 uint32_t* __restrict__ Srow16, FwArgs f) {
-  constexpr int b = FwB<T>::b, R = b / 32;
+  constexpr int b = Fw1<T>::b, RI = Fw1<T>::RI, RJ = Fw1<T>::RJ, U = Fw1<T>::U;
+  static_assert(U % RI == 0 && U % RJ == 0, "round unroll covers both owners");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* rs = reinterpret_cast<T*>(smem_raw);
   T* cT = rs + b * b;
@@ -230,32 +242,31 @@ __global__ void __launch_bounds__(kFw1Threads) fw_phase1_kernel(T* __restrict__ 
   if (threadIdx.x == 0) {
     if (f.group_start) rstore(f, &f.ctrl->s16_overflow[0], 0);
   }
-  T v[R][R];
+  T v[RI][RJ];
   load_block(D, f, f.k0, f.k0, ty, tx, v);
   bool sat = false;
-  for (int kb = 0; kb < b; kb += R) {
-    const int owner = kb / R;
+  for (int kb = 0; kb < b; kb += U) {
 #pragma unroll
-    for (int kk = 0; kk < R; ++kk) {
+    for (int kk = 0; kk < U; ++kk) {
       const int k = kb + kk;
-      if (ty == owner) {
+      if (ty == k / RI) {
 #pragma unroll
-        for (int j = 0; j < R; ++j) rs[k * b + tx * R + j] = v[kk][j];
+        for (int j = 0; j < RJ; ++j) rs[k * b + tx * RJ + j] = v[kk % RI][j];
       }
-      if (tx == owner) {
+      if (tx == k / RJ) {
 #pragma unroll
-        for (int i = 0; i < R; ++i) cT[k * b + ty * R + i] = v[i][kk];
+        for (int i = 0; i < RI; ++i) cT[k * b + ty * RI + i] = v[i][kk % RJ];
       }
       __syncthreads();
-      T rowv[R], colv[R];
+      T rowv[RJ], colv[RI];
 #pragma unroll
-      for (int j = 0; j < R; ++j) rowv[j] = rs[k * b + tx * R + j];
+      for (int j = 0; j < RJ; ++j) rowv[j] = rs[k * b + tx * RJ + j];
 #pragma unroll
-      for (int i = 0; i < R; ++i) colv[i] = cT[k * b + ty * R + i];
+      for (int i = 0; i < RI; ++i) colv[i] = cT[k * b + ty * RI + i];
 #pragma unroll
-      for (int i = 0; i < R; ++i)
+      for (int i = 0; i < RI; ++i)
 #pragma unroll
-        for (int j = 0; j < R; ++j) relax<T, MODE>(v[i][j], colv[i], rowv[j], f.int_mode, f.limit, sat);
+        for (int j = 0; j < RJ; ++j) relax<T, MODE>(v[i][j], colv[i], rowv[j], f.int_mode, f.limit, sat);
     }
   }
   store_block(D, f, f.k0, f.k0, ty, tx, v);
