@@ -21,6 +21,7 @@
 // otherwise the 32-bit kernel; the masked variant (reference screen failed)
 // uses per-candidate overflow masking throughout.
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "btas_gemm.cuh"
@@ -106,6 +107,12 @@ struct FwArgs {
   int panel_mode;    // phase 2 grid: 0 = y selects row (0) / column (1) panels, 1 = rows only, 2 = columns only
   int col_blk0;      // first row block of the column panels (blockIdx.x offset)
   int emit_s16;      // also emit the int16x2 operands
+  // phase 1 ORs its s16 flag into ctrl->s16_overflow[p1_slot]; slot 1 while
+  // it runs concurrently with the thin passes gated on slot 0 (a flip of the
+  // gate word in mid-launch would split a gated pair); the panel kernel that
+  // follows the join folds slot 1 into slot 0 (fold_slot1)
+  int p1_slot;
+  int fold_slot1;
   int32_t* flags;
   FwCtrl* ctrl;
   // fused pivot-panel broadcast (distributed FW): every store into this
@@ -221,6 +228,18 @@ BTAS_D bool emit_history(const T* __restrict__ h, int64_t rc0, int BLK, const Fw
 #define BTAS_FW1_THREADS 512
 #endif
 constexpr int kFw1Threads = BTAS_FW1_THREADS;
+#ifndef BTAS_FW_OVERLAP_P1_MIN_BLOCKS
+#define BTAS_FW_OVERLAP_P1_MIN_BLOCKS 128
+#endif
+constexpr int kOverlapP1MinBlocks = BTAS_FW_OVERLAP_P1_MIN_BLOCKS;  // n >= 16384 at b = 128
+
+// env BTAS_FW_OVERLAP_P1_MIN_BLOCKS overrides the threshold (tests force the
+// overlapped schedule on small graphs; read per call, it is one getenv)
+inline int overlap_p1_min_blocks() {
+  const char* e = getenv("BTAS_FW_OVERLAP_P1_MIN_BLOCKS");
+  const int v = e ? atoi(e) : 0;
+  return v > 0 ? v : kOverlapP1MinBlocks;
+}
 
 template <class T>
 struct Fw1 {
@@ -239,8 +258,9 @@ __global__ void __launch_bounds__(kFw1Threads) fw_phase1_kernel(T* __restrict__ 
   T* rs = reinterpret_cast<T*>(smem_raw);
   T* cT = rs + b * b;
   const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    if (f.group_start) rstore(f, &f.ctrl->s16_overflow[0], 0);
+  if (threadIdx.x == 0 && f.group_start) {
+    rstore(f, &f.ctrl->s16_overflow[0], 0);
+    rstore(f, &f.ctrl->s16_overflow[1], 0);
   }
   T v[RI][RJ];
   load_block(D, f, f.k0, f.k0, ty, tx, v);
@@ -279,7 +299,7 @@ __global__ void __launch_bounds__(kFw1Threads) fw_phase1_kernel(T* __restrict__ 
   bool out16 = emit_history(cT, f.k0 - f.slab_r0, f.BMa, f, Scol, Scol16);  // Scol rows are slab-local
   out16 |= emit_history(rs, f.k0, f.BNb, f, Srow, Srow16);
   if (__syncthreads_or(out16) && threadIdx.x == 0) {
-    rflag_or(f, &f.ctrl->s16_overflow[0]);
+    rflag_or(f, &f.ctrl->s16_overflow[f.p1_slot]);
   }
   if (MODE == kChecked && __any_sync(0xffffffffu, sat) && (threadIdx.x & 31) == 0)
     atomicOr(&f.flags[BTAS_FLAG_SATURATED], 1);
@@ -554,6 +574,9 @@ __global__ void __launch_bounds__(kFwHThreads, 2) fw_panel_half_kernel(T* __rest
   constexpr int b = FwH<T>::b, HR = FwH<T>::HR, LS = FwH<T>::LS, RS = FwH<T>::RS;
   const bool row_panel = blockIdx.y == 0;
   const int blk = (int)(blockIdx.x >> 1), half = (int)(blockIdx.x & 1);
+  if (f.fold_slot1 && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 &&
+      *reinterpret_cast<volatile int32_t*>(&f.ctrl->s16_overflow[1]) != 0)
+    rflag_or(f, &f.ctrl->s16_overflow[0]);
   if (blk == (int)(f.k0 / b)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Ls = reinterpret_cast<T*>(smem_raw);  // Ls[m][i] = left[i][m]
@@ -860,36 +883,44 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
   // tiles and each fills only n/128 CTAs: the column pass runs on a side
   // stream, forked from and joined back into the caller's stream (per host
   // thread and device, created once), so both share the SMs.
-  cudaStream_t side = nullptr;
-  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  cudaStream_t side = nullptr, side2 = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr, join_ev2 = nullptr;
   {
     // created together or not at all (a partial set is destroyed and the
     // device is marked so creation is not retried on every call); they live
     // for the thread's lifetime
-    thread_local cudaStream_t t_side[64] = {};
-    thread_local cudaEvent_t t_fork[64] = {}, t_join[64] = {};
+    thread_local cudaStream_t t_side[64] = {}, t_side2[64] = {};
+    thread_local cudaEvent_t t_fork[64] = {}, t_join[64] = {}, t_join2[64] = {};
     thread_local bool t_failed[64] = {};
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64) {
       if (!t_side[dev] && !t_failed[dev]) {
-        cudaStream_t s = nullptr;
-        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        cudaStream_t s = nullptr, s2 = nullptr;
+        cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
         if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) == cudaSuccess &&
             cudaEventCreateWithFlags(&e0, cudaEventDisableTiming) == cudaSuccess &&
-            cudaEventCreateWithFlags(&e1, cudaEventDisableTiming) == cudaSuccess) {
+            cudaEventCreateWithFlags(&e1, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&e2, cudaEventDisableTiming) == cudaSuccess) {
           t_side[dev] = s;
+          t_side2[dev] = s2;
           t_fork[dev] = e0;
           t_join[dev] = e1;
+          t_join2[dev] = e2;
         } else {
           (void)cudaGetLastError();
+          if (e1) cudaEventDestroy(e1);
           if (e0) cudaEventDestroy(e0);
+          if (s2) cudaStreamDestroy(s2);
           if (s) cudaStreamDestroy(s);
           t_failed[dev] = true;
         }
       }
       side = t_side[dev];
+      side2 = t_side2[dev];
       fork_ev = t_fork[dev];
       join_ev = t_join[dev];
+      join_ev2 = t_join2[dev];
     } else {
       (void)cudaGetLastError();
     }
@@ -912,11 +943,17 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
     }
     ~Join() { (void)close(); }
   };
-  auto phases12 = [&](int kb, int slot) -> int {
+  auto phase1 = [&](int kb, int slot, int p1_slot) -> int {
     f.k0 = (int64_t)kb * b;
     f.koff = slot * b;
     f.group_start = slot == 0;
+    f.p1_slot = p1_slot;
     fw_phase1_kernel<T, MODE><<<1, kFw1Threads, smem1, st>>>(D, rsp, csp, scol, srow, scol16, srow16, f);
+    BTAS_CUDA_CHECK_LAUNCH();
+    return BTAS_OK;
+  };
+  auto phase2 = [&](int fold_slot1) -> int {
+    f.fold_slot1 = fold_slot1;
     if (nblk > 1) {
       if (exact_panels && sizeof(T) == 4)
         fw_panel_half_kernel<T4><<<dim3(2 * nblk, 2), kFwHThreads, FwH<T4>::smem, st>>>(
@@ -927,9 +964,22 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
         fw_phase2_kernel<T, MODE><<<dim3(nblk, 2), kFw2Threads, smem2, st>>>(D, rsp, csp, scol, srow, scol16,
                                                                             srow16, f);
     }
+    f.fold_slot1 = 0;
     BTAS_CUDA_CHECK_LAUNCH();
     return BTAS_OK;
   };
+  auto phases12 = [&](int kb, int slot) -> int {
+    int r = phase1(kb, slot, 0);
+    return r ? r : phase2(0);
+  };
+  // Large graphs: the pivot tile's pending update runs first and phase 1
+  // (one CTA, b dependent rounds) overlaps the rest of the thin passes,
+  // which run on the two side streams with their persistent grids capped
+  // one SM short (the thin passes span several waves there, phase 1 was
+  // serial after them).  Exact-integer panels on 4-byte storage only (the
+  // panel kernel folds phase 1's s16 flag word back in).
+  const bool overlap_p1 = exact_panels && sizeof(T) == 4 && side != nullptr && side2 != nullptr &&
+                          nblk >= overlap_p1_min_blocks();
 
   // Lookahead groups of kLook pivot blocks (4-byte storage, where b equals
   // the GEMM tile edge).  Inside a group, block kb0+j's row and column
@@ -946,6 +996,63 @@ int fw_typed(int integer_mode, T* D, int64_t ld, int64_t n, double max_abs, doub
     for (int j = 0; j < m; ++j) {
       const int kb = kb0 + j;
       const int64_t kk = (int64_t)kb * b, mk = std::min<int64_t>(b, n - kk);
+      if (j > 0 && overlap_p1) {
+        if (cudaEventRecord(fork_ev, st) != cudaSuccess || cudaStreamWaitEvent(side, fork_ev, 0) != cudaSuccess ||
+            cudaStreamWaitEvent(side2, fork_ev, 0) != cudaSuccess) {
+          (void)cudaGetLastError();
+          return BTAS_ERR_CUDA;
+        }
+        Join join1, join2;
+        join1.st = join2.st = st;
+        join1.side = side;
+        join1.ev = join_ev;
+        join2.side = side2;
+        join2.ev = join_ev2;
+        join1.open = join2.open = true;
+        const int sms = device_sm_count();
+        {  // pending updates -> row block kb except the pivot tile (side stream 1)
+          GemmArgs a = g, a16 = g16;
+          a.M = a16.M = mk;
+          a.mblocks = a16.mblocks = 1;
+          a.Ap = static_cast<const T*>(g.Ap) + (size_t)kb * g.Kp2s * G::BMa * 2;
+          a16.Ap = static_cast<const uint32_t*>(g16.Ap) + (size_t)kb * g16.Kp2s * 128 * 2;
+          a.C = a16.C = D + kk * ld;
+          a.Z = a16.Z = D + kk * ld;
+          a.skip_col_lo = a16.skip_col_lo = kk;
+          a.skip_col_hi = a16.skip_col_hi = kk + b;
+          a.max_ctas = a16.max_ctas = sms / 2;
+          if ((rc = phase3_on(a, a16, j, side))) return rc;
+        }
+        {  // pending updates -> column block kb outside the pivot rows (side stream 2)
+          GemmArgs a = g, a16 = g16;
+          a.N = a16.N = mk;
+          a.nblocks = a16.nblocks = 1;
+          a.Bp = static_cast<const T*>(g.Bp) + (size_t)kb * g.Kp2s * G::BNb * 2;
+          a16.Bp = static_cast<const uint32_t*>(g16.Bp) + (size_t)kb * g16.Kp2s * 128 * 2;
+          a.C = a16.C = D + kk;
+          a.Z = a16.Z = D + kk;
+          a.skip_row_lo = a16.skip_row_lo = kk;
+          a.skip_row_hi = a16.skip_row_hi = kk + b;
+          a.max_ctas = a16.max_ctas = sms - 1 - sms / 2;
+          if ((rc = phase3_on(a, a16, j, side2))) return rc;
+        }
+        {  // pending updates -> the pivot tile, then phase 1, on the caller's stream
+          GemmArgs a = g, a16 = g16;
+          a.M = a16.M = a.N = a16.N = mk;
+          a.mblocks = a16.mblocks = a.nblocks = a16.nblocks = 1;
+          a.Ap = static_cast<const T*>(g.Ap) + (size_t)kb * g.Kp2s * G::BMa * 2;
+          a16.Ap = static_cast<const uint32_t*>(g16.Ap) + (size_t)kb * g16.Kp2s * 128 * 2;
+          a.Bp = static_cast<const T*>(g.Bp) + (size_t)kb * g.Kp2s * G::BNb * 2;
+          a16.Bp = static_cast<const uint32_t*>(g16.Bp) + (size_t)kb * g16.Kp2s * 128 * 2;
+          a.C = a16.C = D + kk * ld + kk;
+          a.Z = a16.Z = D + kk * ld + kk;
+          if ((rc = phase3(a, a16, j))) return rc;
+        }
+        if ((rc = phase1(kb, j, 1))) return rc;
+        if ((rc = join1.close()) || (rc = join2.close())) return rc;
+        if ((rc = phase2(1))) return rc;
+        continue;
+      }
       if (j > 0) {
         const bool fork = side != nullptr;
         Join join;

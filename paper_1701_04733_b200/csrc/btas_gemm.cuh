@@ -60,6 +60,7 @@ struct GemmArgs {
   int64_t skip_row_lo, skip_row_hi, skip_col_lo, skip_col_hi;
   int64_t Kp2s;          // k-pair stride between blocks of the packed buffers (0: = Kp2)
   int no_diag;           // 1: skip the diag<0 test (C is a window, not the whole matrix)
+  int max_ctas;          // > 0: cap the persistent grid (leave SMs to a concurrent latency-bound chain)
   // fused all-gather: every output element is also stored, at the same
   // offset, into up to kMaxPeers other buffers — the other ranks' copies
   // mapped into this process (NVLink peer memory), so the exchange of
@@ -791,7 +792,9 @@ int launch_gemm_epi(const GemmArgs& g, cudaStream_t stream) {
   }
   if (g.Kp2 < P::KP || g.Kp2 % P::KP != 0) return BTAS_ERR_INVALID;  // whole pipeline stages only
   const int ntiles = g.mblocks * g.nblocks;
-  const int grid = ntiles < device_sm_count() ? ntiles : device_sm_count();
+  int cap = device_sm_count();
+  if (g.max_ctas > 0 && g.max_ctas < cap) cap = g.max_ctas;
+  const int grid = ntiles < cap ? ntiles : cap;
   if (grid <= 0) return BTAS_OK;
   tropical_gemm_kernel<P, MIN, EPI><<<grid, kGemmThreads, S::smem_bytes, stream>>>(g);
   BTAS_CUDA_CHECK_LAUNCH();

@@ -135,6 +135,51 @@ def test_fw_equals_squaring_midsize(cuda, dtype, n):
     assert got.tobytes() == want.tobytes()
 
 
+@pytest.mark.parametrize("dtype", [torch.int32, torch.float32])
+def test_fw_overlapped_phase1_schedule(cuda, dtype, monkeypatch):
+    """The large-graph schedule (pivot tile first, phase 1 concurrent with the
+    capped thin passes on two side streams, phase 1's s16 flag in its own
+    word folded back by the panel kernel) forced onto small graphs: the same
+    bytes as the serial schedule and as squaring — ragged last pivot blocks,
+    several lookahead groups, and weights whose panels leave the s16 domain
+    in mid-group (the gate of the next thin passes must see it)."""
+    monkeypatch.setenv("BTAS_FW_SQUARING_MAX_N", "0")
+    for n, wr, seed in ((700, (1, 100), 1), (1500, (1, 100), 2), (1100, (1, 3000), 3), (1300, (1, 40000), 4)):
+        adj = random_graph_matrix(n, 0.3, wr, 777 + seed, dtype=dtype)
+        monkeypatch.setenv("BTAS_FW_OVERLAP_P1_MIN_BLOCKS", "1000000")
+        serial = bt.floyd_warshall(adj)
+        monkeypatch.setenv("BTAS_FW_OVERLAP_P1_MIN_BLOCKS", "2")
+        over = bt.floyd_warshall(adj)
+        assert not over.negative_cycle and not serial.negative_cycle
+        assert over.distances.dist == serial.distances.dist, (n, wr)
+        assert over.distances.dist == bt.apsp_by_squaring(adj).distances.dist, (n, wr)
+    # s16-domain weights except inside pivot block 5, which is cut off from
+    # blocks 0-4 and whose internal edges weigh 40000: only block 5's CLOSED
+    # pivot tile (phase 1's emission) leaves the s16 domain, its panels stay
+    # inside, so the flag word phase 1 sets concurrently with the thin passes
+    # is the only signal that block 6's thin passes (whose column block 5
+    # reads that tile) must run the 32-bit kernel (int16 lanes would wrap)
+    n = 1200
+    sym = np.concatenate([b for _, b in dense_rows(n, 0.3, (1, 100), 99)])
+    sym[640:768, :640] = math.inf
+    sym[:640, 640:768] = math.inf
+    rng = np.random.default_rng(5)
+    sym[640:768, 768:] = rng.integers(1, 100, (128, n - 768))  # every panel entry has a short direct edge
+    sym[768:, 640:768] = rng.integers(1, 100, (n - 768, 128))
+    inner = sym[640:768, 640:768]
+    inner[np.isfinite(inner) & (inner > 0)] = 40000
+    adj = bt.TropicalMatrix(MIN, sym, dtype=dtype)
+    monkeypatch.setenv("BTAS_FW_OVERLAP_P1_MIN_BLOCKS", "1000000")
+    serial = bt.floyd_warshall(adj)
+    monkeypatch.setenv("BTAS_FW_OVERLAP_P1_MIN_BLOCKS", "2")
+    over = bt.floyd_warshall(adj)
+    assert over.distances.dist == serial.distances.dist
+    rows = [0, 650, 700, 800, n - 1]
+    want = ot.closure_rows(sym, rows, STORAGE[dtype], True,
+                           gemm=lambda a, b: on.matmul(a, b, "minplus", STORAGE[dtype], True)[0])
+    assert over.distances.dist.to_numpy()[rows].tobytes() == want.tobytes()
+
+
 @pytest.mark.parametrize("dtype", DTYPES)
 def test_fw_negative_weights_and_sparse(cuda, dtype):
     """Negative weights without negative cycles (no s16 shortcut for the
