@@ -113,6 +113,12 @@ struct FwArgs {
   // follows the join folds slot 1 into slot 0 (fold_slot1)
   int p1_slot;
   int fold_slot1;
+  // exact-integer distributed program: phase 1 writes the CLOSED pivot tile
+  // T* (row-major, b x b) to its row-snapshot buffer (the broadcast slot)
+  // instead of the row history, and column panels of ranks that do not hold
+  // the pivot rows read T* from there (tstar) instead of from D
+  int tstar_out;
+  const void* tstar;
   int32_t* flags;
   FwCtrl* ctrl;
   // fused pivot-panel broadcast (distributed FW): every store into this
@@ -290,9 +296,15 @@ __global__ void __launch_bounds__(kFw1Threads) fw_phase1_kernel(T* __restrict__ 
     }
   }
   store_block(D, f, f.k0, f.k0, ty, tx, v);
+  if (f.tstar_out) {  // the closed tile, row-major (padding rows/cols hold Infinity)
+#pragma unroll
+    for (int i = 0; i < RI; ++i)
+#pragma unroll
+      for (int j = 0; j < RJ; ++j) rstore(f, rowsnapP + (ty * RI + i) * b + tx * RJ + j, v[i][j]);
+  }
   __syncthreads();
   for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
-    rstore(f, rowsnapP + e, rs[e]);
+    if (!f.tstar_out) rstore(f, rowsnapP + e, rs[e]);
     rstore(f, colsnapT + e, cT[e]);
   }
   // pivot rows of Scol (A operand) and pivot columns of Srow (B operand)
@@ -572,8 +584,8 @@ __global__ void __launch_bounds__(kFwHThreads, 2) fw_panel_half_kernel(T* __rest
                                                                        uint32_t* __restrict__ Srow16, FwArgs f) {
   static_assert(sizeof(T) == 4, "b = 128 storage");
   constexpr int b = FwH<T>::b, HR = FwH<T>::HR, LS = FwH<T>::LS, RS = FwH<T>::RS;
-  const bool row_panel = blockIdx.y == 0;
-  const int blk = (int)(blockIdx.x >> 1), half = (int)(blockIdx.x & 1);
+  const bool row_panel = f.panel_mode == 0 ? blockIdx.y == 0 : f.panel_mode == 1;
+  const int blk = (row_panel ? 0 : f.col_blk0) + (int)(blockIdx.x >> 1), half = (int)(blockIdx.x & 1);
   if (f.fold_slot1 && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 &&
       *reinterpret_cast<volatile int32_t*>(&f.ctrl->s16_overflow[1]) != 0)
     rflag_or(f, &f.ctrl->s16_overflow[0]);
@@ -591,8 +603,11 @@ __global__ void __launch_bounds__(kFwHThreads, 2) fw_panel_half_kernel(T* __rest
   const int64_t lr0 = (row_panel ? f.k0 : r0) + half * HR;
   const int64_t rc0 = row_panel ? c0 : f.k0;
   auto at = [&](int64_t row, int64_t col) -> T {
-    return (row < f.n && col < f.n) ? D[(row - f.slab_r0) * f.ld + col] : inf;
+    return (row < f.slab_r1 && col < f.n) ? D[(row - f.slab_r0) * f.ld + col] : inf;
   };
+  // the right operand of a column panel is T*: from D, or from the
+  // broadcast copy when this rank does not hold the pivot rows
+  const T* tstar = (!row_panel && f.tstar) ? static_cast<const T*>(f.tstar) : nullptr;
   {  // left operand: a warp reads 4 rows x 8 columns (four full 32-byte
      // sectors) and stores them transposed into 32 distinct banks
     constexpr int kQ = HR * b / 32 / (kFwHThreads / 32);  // patches per warp
@@ -619,7 +634,9 @@ __global__ void __launch_bounds__(kFwHThreads, 2) fw_panel_half_kernel(T* __rest
       const int e = (int)threadIdx.x + kFwHThreads * q;
       const int m = e >> 5, x = 4 * (e & 31);
       const int64_t row = f.k0 + m;
-      if (vec && row < f.n) {
+      if (tstar != nullptr) {
+        v[q] = *reinterpret_cast<const uint4*>(tstar + m * b + x);
+      } else if (vec && row < f.slab_r1) {
         v[q] = *reinterpret_cast<const uint4*>(D + (row - f.slab_r0) * f.ld + rc0 + x);
       } else {
         v[q].x = __builtin_bit_cast(uint32_t, at(row, rc0 + x));
@@ -663,7 +680,7 @@ __global__ void __launch_bounds__(kFwHThreads, 2) fw_panel_half_kernel(T* __rest
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int x = lane + 32 * j;
-      if (row < f.n && c0 + x < f.n) D[(row - f.slab_r0) * f.ld + c0 + x] = acc[i][j];
+      if (row < f.slab_r1 && c0 + x < f.n) D[(row - f.slab_r0) * f.ld + c0 + x] = acc[i][j];
       if (row_panel) h[(w * 8 + i) * RS + x] = acc[i][j];  // h[k - 64 half][x]
     }
   }
@@ -1160,6 +1177,7 @@ int fw_dist_group_typed(int integer_mode, int stage, T* D, int64_t ld, int64_t n
                         int64_t slab_rows, int64_t kb0, int m, int32_t* flags, unsigned char* ws, void* const* peers,
                         int n_peers, cudaStream_t st) {
   using G = FwGeom<T>;
+  using T4 = std::conditional_t<sizeof(T) == 4, T, float>;  // the half-tile panel kernel's storage
   constexpr int b = G::b, kLook = G::look;
   constexpr bool CHECKED = MODE == kChecked;
   const FwDistWs W = fw_dist_ws<T>(n, slab_rows);
@@ -1212,12 +1230,20 @@ int fw_dist_group_typed(int integer_mode, int stage, T* D, int64_t ld, int64_t n
     if (cudaFuncSetAttribute(fw_phase1_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
             cudaSuccess ||
         cudaFuncSetAttribute(fw_phase2_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2) !=
-            cudaSuccess) {
+            cudaSuccess ||
+        (sizeof(T) == 4 && cudaFuncSetAttribute(fw_panel_half_kernel<T4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)FwH<T4>::smem) != cudaSuccess)) {
       (void)cudaGetLastError();
       return BTAS_ERR_CUDA;
     }
     mark_configured(configured);
   }
+  // int32 storage without negative weights: the exact-integer panel products
+  // (fw_panel_half_kernel) as in btas_fw; phase 1 broadcasts the closed pivot
+  // tile T* in the row-snapshot slot, from which the other ranks' column
+  // panels read it
+  const bool exact = MODE == kFast && !CHECKED && Traits<T>::dtype == BTAS_I32;
+  f.tstar_out = exact ? 1 : 0;
 
   // GEMM descriptors over this rank's slab (rows slab-local); per launch only
   // the k range (slots), the row/column window and the skips change
@@ -1294,8 +1320,14 @@ int fw_dist_group_typed(int integer_mode, int stage, T* D, int64_t ld, int64_t n
     fc.col_blk0 = (int)(slab_r0 / b);
     fc.n_peers = 0;  // column panels are rank-local
     const int nsb = (int)ceil_div(slab_rows, b);
-    fw_phase2_kernel<T, MODE><<<dim3(nsb, 1), kFw2Threads, smem2, st>>>(D, rsp + (size_t)j * b * b, csp, scol, srow,
-                                                                       scol16, srow16, fc);
+    if (exact) {
+      fc.tstar = owner ? nullptr : rsp + (size_t)j * b * b;  // the owner's column panel reads T* from D
+      fw_panel_half_kernel<T4><<<dim3(2 * nsb, 1), kFwHThreads, FwH<T4>::smem, st>>>(
+          reinterpret_cast<T4*>(D), reinterpret_cast<T4*>(scol), reinterpret_cast<T4*>(srow), scol16, srow16, fc);
+    } else {
+      fw_phase2_kernel<T, MODE><<<dim3(nsb, 1), kFw2Threads, smem2, st>>>(D, rsp + (size_t)j * b * b, csp, scol,
+                                                                         srow, scol16, srow16, fc);
+    }
     BTAS_CUDA_CHECK_LAUNCH();
     return BTAS_OK;
   };
@@ -1334,8 +1366,13 @@ int fw_dist_group_typed(int integer_mode, int stage, T* D, int64_t ld, int64_t n
         fw_phase1_kernel<T, MODE><<<1, kFw1Threads, smem, st>>>(D, rsp_j, csp, scol, srow, scol16, srow16, fp);
         if (nblk > 1) {
           fp.panel_mode = 1;
-          fw_phase2_kernel<T, MODE><<<dim3(nblk, 1), kFw2Threads, smem2, st>>>(D, rsp_j, csp, scol, srow, scol16,
-                                                                              srow16, fp);
+          if (exact)
+            fw_panel_half_kernel<T4><<<dim3(2 * nblk, 1), kFwHThreads, FwH<T4>::smem, st>>>(
+                reinterpret_cast<T4*>(D), reinterpret_cast<T4*>(scol), reinterpret_cast<T4*>(srow), scol16, srow16,
+                fp);
+          else
+            fw_phase2_kernel<T, MODE><<<dim3(nblk, 1), kFw2Threads, smem2, st>>>(D, rsp_j, csp, scol, srow, scol16,
+                                                                                srow16, fp);
         }
         BTAS_CUDA_CHECK_LAUNCH();
         if ((rc = cols_panel(kb, j))) return rc;
