@@ -180,6 +180,16 @@ def test_fw_overlapped_phase1_schedule(cuda, dtype, monkeypatch):
     assert over.distances.dist.to_numpy()[rows].tobytes() == want.tobytes()
 
 
+def test_fw_overlapped_phase1_at_scale(cuda):
+    """n = 16384 (128 pivot blocks: the overlapped phase-1 schedule is on by
+    default) with weights that straddle the s16 domain, so the int16x2 gate
+    flips inside lookahead groups: FW bytes == repeated squaring bytes."""
+    adj = random_graph_matrix(16384, 0.02, (1, 3000), 5151, dtype=torch.int32)
+    fw = bt.floyd_warshall(adj)
+    sq = bt.apsp_by_squaring(adj)
+    assert not fw.negative_cycle and fw.distances.dist == sq.distances.dist
+
+
 @pytest.mark.parametrize("dtype", DTYPES)
 def test_fw_negative_weights_and_sparse(cuda, dtype):
     """Negative weights without negative cycles (no s16 shortcut for the
